@@ -1,0 +1,219 @@
+"""Seeded synthetic inputs for the BASELINE.json configurations 0-4.
+
+This module holds NO arithmetic of the IB-GM method: it only builds initial
+conditions (fluid velocity on the MAC faces, membrane geometry, force-connection
+lists).  Both the CUDA path (tests, bench.py) and the oracle consume it; it
+imports neither.  Recipes are stated in DESIGN.md ("Inputs") and follow SURVEY.md
+8(c) readings R8, R10, R11, R15, R19.
+
+Array convention: fields are numpy arrays indexed [j][i] (2D) or [k][j][i] (3D),
+x fastest, so the flat index is i + N*(j + N*k).  u lives at (i h, (j+1/2) h, ...),
+v at ((i+1/2) h, j h, ...), w at (..., k h).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+COS4 = 0      # 4-point cosine delta (BASELINE.json configs)
+PESKIN4 = 1   # paper eq. (discretedelta)
+
+
+@dataclass
+class Problem:
+    name: str
+    dim: int
+    n: int
+    mu: float
+    rho: float
+    dt: float
+    steps: int
+    kernel: int = COS4
+    chi: float = 0.6
+    u: List[np.ndarray] = field(default_factory=list)     # dim arrays
+    p: Optional[np.ndarray] = None
+    X: np.ndarray = None          # [npts][dim]
+    edges: np.ndarray = None      # [nedges][2] int64
+    kappa: np.ndarray = None      # [nedges]
+    rest: Optional[np.ndarray] = None
+    weight: np.ndarray = None     # [npts]
+
+    @property
+    def ncell(self) -> int:
+        return self.n ** self.dim
+
+    @property
+    def npts(self) -> int:
+        return 0 if self.X is None else self.X.shape[0]
+
+
+# ------------------------------------------------------------------ geometry
+def ellipse_fibre(npts: int, center, axes, sigma: float = 1.0):
+    """Closed fibre X_k = c + (a cos 2 pi s_k, b sin 2 pi s_k), s_k = k/npts
+    (uniform in s: R8).  Returns X, ring edges, kappa = sigma/h_s^2,
+    weight = h_s (R9)."""
+    s = np.arange(npts, dtype=np.float64) / npts
+    X = np.stack([center[0] + axes[0] * np.cos(2 * np.pi * s),
+                  center[1] + axes[1] * np.sin(2 * np.pi * s)], axis=1)
+    k = np.arange(npts, dtype=np.int64)
+    edges = np.stack([k, (k + 1) % npts], axis=1)
+    hs = 1.0 / npts
+    kappa = np.full(npts, sigma / hs ** 2)
+    weight = np.full(npts, hs)
+    return X, edges, kappa, weight
+
+
+def fibonacci_sphere(npts: int) -> np.ndarray:
+    """Near-uniform unit-sphere point set (R11)."""
+    i = np.arange(npts, dtype=np.float64)
+    z = 1.0 - (2.0 * i + 1.0) / npts
+    r = np.sqrt(np.maximum(0.0, 1.0 - z * z))
+    golden = np.pi * (3.0 - np.sqrt(5.0))
+    th = golden * i
+    return np.stack([r * np.cos(th), r * np.sin(th), z], axis=1)
+
+
+def random_rotation(rng: np.random.Generator) -> np.ndarray:
+    """Uniform random 3x3 rotation from a seeded generator (QR of a Gaussian matrix)."""
+    A = rng.standard_normal((3, 3))
+    Q, R = np.linalg.qr(A)
+    Q = Q * np.sign(np.diag(R))
+    if np.linalg.det(Q) < 0:
+        Q[:, 0] = -Q[:, 0]
+    return Q
+
+
+def sphere_triangulation_edges(P: np.ndarray) -> np.ndarray:
+    """Unique edges of the convex hull triangulation of points on the unit sphere."""
+    from scipy.spatial import ConvexHull
+    hull = ConvexHull(P)
+    t = hull.simplices.astype(np.int64)
+    e = np.concatenate([t[:, [0, 1]], t[:, [1, 2]], t[:, [2, 0]]], axis=0)
+    e.sort(axis=1)
+    e = np.unique(e, axis=0)
+    return e
+
+
+def ellipsoid_shell(nodes: int, center, axes, rng: np.random.Generator, sigma: float = 1.0):
+    """Triangulated ellipsoidal shell (R10, R11): Fibonacci sphere, seeded random
+    rotation, convex-hull edges, scaled to the semi-axes.  Edge springs kappa = sigma,
+    rest length 0, nodal weight 1."""
+    P = fibonacci_sphere(nodes) @ random_rotation(rng).T
+    edges = sphere_triangulation_edges(P)
+    X = np.asarray(center, np.float64)[None, :] + P * np.asarray(axes, np.float64)[None, :]
+    kappa = np.full(edges.shape[0], float(sigma))
+    weight = np.ones(nodes)
+    return X, edges, kappa, weight
+
+
+def _nonoverlapping_centres(rng, count, lo, hi, dim, radius, margin, max_tries=100000):
+    """Rejection-sample `count` centres in [lo,hi]^dim with |c_i - c_j| > r_i + r_j + margin (R19)."""
+    cs: list = []
+    tries = 0
+    while len(cs) < count:
+        tries += 1
+        if tries > max_tries:
+            raise RuntimeError("could not place non-overlapping bodies")
+        c = rng.uniform(lo, hi, size=dim)
+        if all(np.linalg.norm(c - cj) > radius[len(cs)] + radius[j] + margin for j, cj in enumerate(cs)):
+            cs.append(c)
+    return np.array(cs)
+
+
+# ------------------------------------------------------------------ fluid
+def _band_limited(rng, shape, K):
+    """Real random field with Gaussian Fourier coefficients on integer wavenumbers
+    0 < |k| <= K (R15)."""
+    n = shape[0]
+    dim = len(shape)
+    ks = [np.fft.fftfreq(n, 1.0 / n)] * (dim - 1) + [np.fft.rfftfreq(n, 1.0 / n)]
+    grids = np.meshgrid(*ks, indexing="ij")
+    k2 = sum(g * g for g in grids)
+    mask = (k2 > 0) & (k2 <= K * K)
+    coef = (rng.standard_normal(k2.shape) + 1j * rng.standard_normal(k2.shape)) * mask
+    return np.fft.irfftn(coef, s=shape, axes=tuple(range(dim)))
+
+
+def random_divfree(dim: int, n: int, K: int, amp: float, seed: int):
+    """Random discretely divergence-free MAC velocity (R15): the discrete curl of a
+    band-limited random potential (2D stream function at cell corners, 3D vector
+    potential on cell edges), so the MAC divergence vanishes to rounding; scaled so
+    that max_c max|u_c| = amp.  Arrays [j][i] / [k][j][i]."""
+    rng = np.random.default_rng(seed)
+    h = 1.0 / n
+    shape = (n,) * dim
+    # forward difference along grid axis a of a [.., j, i] array: axis index = dim-1-a
+    def fd(q, a):
+        ax = dim - 1 - a
+        return (np.roll(q, -1, axis=ax) - q) / h
+    if dim == 2:
+        A = _band_limited(rng, shape, K)
+        u = [fd(A, 1), -fd(A, 0)]
+    else:
+        Ax, Ay, Az = (_band_limited(rng, shape, K) for _ in range(3))
+        u = [fd(Az, 1) - fd(Ay, 2), fd(Ax, 2) - fd(Az, 0), fd(Ay, 0) - fd(Ax, 1)]
+    m = max(np.abs(c).max() for c in u)
+    return [np.ascontiguousarray(c * (amp / m)) for c in u]
+
+
+# ------------------------------------------------------------------ configs
+def config(idx: int, **over) -> Problem:
+    """BASELINE.json configs[idx]; keyword overrides (n=, nodes=, pts=, steps=) give
+    scaled-down variants for tests.  Seeds: 13051.. (DESIGN.md Inputs)."""
+    if idx == 0:
+        n = over.get("n", 32)
+        pts = over.get("pts", 128)
+        pr = Problem("cfg0", 2, n, 0.01, 1.0, over.get("dt", 1e-3), over.get("steps", 20))
+        pr.u = [np.zeros((n, n)), np.zeros((n, n))]
+        pr.X, pr.edges, pr.kappa, pr.weight = ellipse_fibre(pts, (0.5, 0.5), (0.2, 0.15))
+    elif idx == 1:
+        n = over.get("n", 256)
+        pts = over.get("pts", 1024)
+        pr = Problem("cfg1", 2, n, 0.01, 1.0, over.get("dt", 1e-4), over.get("steps", 200))
+        pr.u = random_divfree(2, n, 8, 0.05, seed=13051)
+        pr.X, pr.edges, pr.kappa, pr.weight = ellipse_fibre(pts, (0.5, 0.5), (0.2, 0.15))
+    elif idx == 2:
+        n = over.get("n", 1024)
+        pts = over.get("pts", 2048)
+        pr = Problem("cfg2", 2, n, 0.005, 1.0, over.get("dt", 2e-5), over.get("steps", 100))
+        pr.u = [np.zeros((n, n)), np.zeros((n, n))]
+        rng = np.random.default_rng(13052)
+        axes = rng.uniform(0.05, 0.12, size=(4, 2))
+        cen = _nonoverlapping_centres(rng, 4, 0.2, 0.8, 2, axes.max(axis=1), 4.0 / n)
+        parts = [ellipse_fibre(pts, cen[b], axes[b]) for b in range(4)]
+        pr.X, pr.edges, pr.kappa, pr.weight = _concat(parts)
+    elif idx == 3:
+        n = over.get("n", 128)
+        nodes = over.get("nodes", 40000)
+        pr = Problem("cfg3", 3, n, 0.01, 1.0, over.get("dt", 1e-4), over.get("steps", 100))
+        pr.u = [np.zeros((n, n, n)) for _ in range(3)]
+        rng = np.random.default_rng(13053)
+        pr.X, pr.edges, pr.kappa, pr.weight = ellipsoid_shell(nodes, (0.5, 0.5, 0.5), (0.2, 0.15, 0.15), rng)
+    elif idx == 4:
+        n = over.get("n", 384)
+        nodes = over.get("nodes", 100000)
+        pr = Problem("cfg4", 3, n, 0.005, 1.0, over.get("dt", 5e-5), over.get("steps", 20))
+        pr.u = random_divfree(3, n, 6, 0.02, seed=13054)
+        rng = np.random.default_rng(13055)
+        axes = rng.uniform(0.05, 0.1, size=(8, 3))
+        cen = _nonoverlapping_centres(rng, 8, 0.15, 0.85, 3, axes.max(axis=1), 4.0 / n)
+        parts = [ellipsoid_shell(nodes, cen[b], axes[b], rng) for b in range(8)]
+        pr.X, pr.edges, pr.kappa, pr.weight = _concat(parts)
+    else:
+        raise ValueError(f"no config {idx}")
+    pr.p = np.zeros_like(pr.u[0])
+    if "kernel" in over:
+        pr.kernel = over["kernel"]
+    return pr
+
+
+def _concat(parts):
+    Xs, Es, Ks, Ws = [], [], [], []
+    off = 0
+    for X, E, K, W in parts:
+        Xs.append(X); Es.append(E + off); Ks.append(K); Ws.append(W)
+        off += X.shape[0]
+    return (np.ascontiguousarray(np.concatenate(Xs)), np.ascontiguousarray(np.concatenate(Es)),
+            np.concatenate(Ks), np.concatenate(Ws))
