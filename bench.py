@@ -1,0 +1,310 @@
+#!/usr/bin/env python
+"""bench.py -- fluid+IB grid-point updates per second (fp64) of the IB-GM step on B200.
+
+Default workload: BASELINE.json configs[3] (3D, 128^3 MAC grid, one triangulated
+ellipsoidal shell of ~40k nodes, rho=1, mu=0.01, dt=1e-4) -- the largest
+configuration that is defined for a single GPU (configs[4] is the 8-GPU z-slab
+case); see DESIGN.md "Measurement".  One "step" = one full IB-GM time step
+(Steps 1a-3f) on the whole grid.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C]
+
+Prints ONE JSON line on rank 0.  value = N^3 * steps * ranks / (max over ranks of the
+device time of the K timed steps).  Inputs (17 resident fp64 fields, ~285 MB at 128^3)
+are larger than the 126 MB L2, so no explicit L2 flush is done between steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fluid+IB grid-point updates/sec (fp64)"
+UNIT = "grid-point updates/s"
+
+# algorithmic HBM bytes per grid cell of each phase:
+# doubles each phase must read + write once, x 8 B.
+ALG_DOUBLES = {
+    3: {"s1_rhs_xsweep": 17, "visc_y": 9, "visc_z": 9, "div": 9, "psi_z": 2, "psi_y": 2, "psi_x_p": 4,
+        "zero_f": 3},
+    2: {"s1_rhs_xsweep": 12, "visc_y": 6, "div": 7, "psi_y": 2, "psi_x_p": 4, "zero_f": 2},
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap", "utilization.gpu"]
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:  # noqa: BLE001
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        time.sleep(0.1)
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:  # noqa: BLE001
+                self.proc.kill()
+
+    def summary(self):
+        sm, smax, reasons, util = [], [], set(), []
+        for l in self.lines:
+            parts = [x.strip() for x in l.split(",")]
+            if len(parts) < len(self.FIELDS):
+                continue
+            try:
+                s, m = float(parts[0]), float(parts[1])
+            except ValueError:
+                continue
+            u = float(parts[6]) if parts[6].replace(".", "").isdigit() else 0.0
+            util.append(u)
+            if u > 0:
+                sm.append(s)
+            smax.append(m)
+            for nm, v in zip(self.NAMES, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(self.lines), "samples_under_load": len(sm)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def cpu_baseline(cfg, steps=2):
+    """The oracle as it stands, single-threaded, on a bounded sample: `steps` full
+    time steps of the same workload (after one untimed step)."""
+    from oracle import oracle as O
+    from paper_1305_3976_b200 import inputs
+    pr = inputs.config(cfg)
+    o = O.Oracle(pr.dim, pr.n, pr.mu, pr.rho, pr.dt, chi=pr.chi, kernel=pr.kernel)
+    o.set_fields(*pr.u, p=pr.p) if pr.dim == 3 else o.set_fields(pr.u[0], pr.u[1], None, pr.p)
+    o.set_boundary(pr.X, pr.edges, pr.kappa, rest=pr.rest, weight=pr.weight)
+    o.step(1)
+    t0 = time.perf_counter()
+    o.step(steps)
+    dt = time.perf_counter() - t0
+    return {"value": pr.ncell * steps / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{steps} full oracle time steps of config {cfg} ({pr.n}^{pr.dim} cells, "
+                      f"{pr.npts} IB points) after 1 untimed step; single-threaded C (oracle/ibgm_oracle.c)",
+            "seconds": dt}
+
+
+def run_reference(args):
+    """--impl reference: the oracle (this tier's reference arm) timed on the host."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    from paper_1305_3976_b200 import inputs
+    pr = inputs.config(args.config)
+    o = O.Oracle(pr.dim, pr.n, pr.mu, pr.rho, pr.dt, chi=pr.chi, kernel=pr.kernel)
+    o.set_fields(*pr.u, p=pr.p) if pr.dim == 3 else o.set_fields(pr.u[0], pr.u[1], None, pr.p)
+    o.set_boundary(pr.X, pr.edges, pr.kappa, rest=pr.rest, weight=pr.weight)
+    t0 = time.perf_counter()
+    o.step(1)                       # one warm-up step (the oracle has no warm-up effects)
+    t1 = time.perf_counter() - t0
+    budget = 150.0                  # keep the whole run within a few minutes
+    k = max(1, min(args.steps, int(budget / max(t1, 1e-3))))
+    t0 = time.perf_counter()
+    o.step(k)
+    dt = time.perf_counter() - t0
+    v = pr.ncell * k / dt
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+           "steps": k, "warmup": 1, "ms_per_step": 1e3 * dt / k, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": f"configs[{args.config}]", "grid": f"{pr.n}^{pr.dim}", "ib_points": pr.npts},
+           "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                            "sample": f"{k} of the requested {args.steps} oracle steps (bounded to ~{budget:.0f} s)"},
+           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import numpy as np
+    import torch
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    from paper_1305_3976_b200 import ibgm, inputs
+    pr = inputs.config(args.config)
+    dim, n = pr.dim, pr.n
+    stream = torch.cuda.current_stream()
+    ctx = ibgm.from_problem(pr, device=local, stream=stream.cuda_stream)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    # warm-up
+    for _ in range(args.warmup):
+        ctx.step(1)
+    ctx.sync()
+    torch.cuda.synchronize()
+
+    # --- timed region A: K steps, device time between two events on the library's stream
+    l0 = ctx.stats()["kernel_launches"]
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            ctx.step(1)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    launches = ctx.stats()["kernel_launches"] - l0
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    updates = float(pr.ncell) * args.steps * world
+    value = updates / (ms * 1e-3)
+
+    # --- timed region B: the same K steps with per-phase event pairs (roofline attribution)
+    ctx.set_profiling(True)
+    kb = max(10, min(args.steps, 200))
+    ctx.step(kb)
+    ctx.sync()
+    ph = ctx.phase_times()
+    ctx.set_profiling(False)
+    tot_ph = sum(v[0] for v in ph.values())
+    dom = max((k for k in ph if k in ALG_DOUBLES[dim]), key=lambda k: ph[k][0])
+    dom_ms = ph[dom][0] / ph[dom][1]
+    alg = ALG_DOUBLES[dim][dom] * 8 * pr.ncell
+    peak, peak_src = measured_peaks()
+    achieved = alg / (dom_ms * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"traffic_cfg{args.config}.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(dom)
+    step_alg = sum(ALG_DOUBLES[dim][k] for k in ALG_DOUBLES[dim] if k in ph) * 8 * pr.ncell
+    phases = {k: {"ms": round(v[0] / v[1], 5), "share": round(v[0] / tot_ph, 4),
+                  "alg_gbs": (round(ALG_DOUBLES[dim][k] * 8 * pr.ncell / (v[0] / v[1] * 1e-3) / 1e9, 1)
+                              if k in ALG_DOUBLES[dim] else None)} for k, v in ph.items()}
+
+    # --- e2e through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda shape: torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()  # noqa: E731
+        hu = [pin(ctx.shape) for _ in range(dim)]
+        hp = pin(ctx.shape)
+        hX = pin((pr.npts, dim))
+        ctx.get_fields_into(hu[0], hu[1], hu[2] if dim == 3 else None, hp, hX)
+        ke = max(3, min(args.steps, 20))
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(ke):
+            ctx.set_fields(hu[0], hu[1], hu[2] if dim == 3 else None, hp)   # H2D of the step's inputs
+            ctx.step(1)
+            ctx.get_fields_into(hu[0], hu[1], hu[2] if dim == 3 else None, hp, hX)  # D2H of the result
+        f1.record(stream)
+        torch.cuda.synchronize()
+        ems = f0.elapsed_time(f1)
+        if world > 1:
+            t = torch.tensor([ems], device="cuda")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": float(pr.ncell) * ke * world / (ems * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": (dim + 1) * pr.ncell * 8,
+               "d2h_bytes_per_step": (dim + 1) * pr.ncell * 8 + pr.npts * dim * 8,
+               "steps": ke, "note": "per step: ib_set_fields (H2D u,v,[w],p from pinned) + ib_step(1) + "
+                                    "ib_get_fields (D2H u,v,[w],p,X to pinned)"}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args.config, steps=2 if pr.ncell <= 4_000_000 else 1)
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak" if world > 1 else "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"configs[{args.config}]", "grid": f"{n}^{dim}", "ib_points": pr.npts,
+                       "ib_edges": int(pr.edges.shape[0]), "mu": pr.mu, "rho": pr.rho, "dt": pr.dt,
+                       "delta_kernel": "cos4", "parallelism": "single-gpu" if world == 1 else f"replicas{world}",
+                       "l2": "inputs larger than L2 (17 resident fp64 fields), no flush"},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "alg_bytes_per_launch": alg, "peak_source": peak_src,
+                         "step_frac": step_alg / (ms / args.steps * 1e-3) / 1e9 / peak},
+            "phases": phases,
+            "gpu_launches": launches,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(out), flush=True)
+    ctx.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,172 @@
+/*
+ * ibgm.h -- C-ABI of the B200-native IB-GM hot path.
+ *
+ * The method: the immersed-boundary / Guermond-Minev (IB-GM) time step of
+ * Wiens & Stockie, "An Efficient Parallel Immersed Boundary Algorithm using a
+ * Pseudo-Compressible Fluid Solver", arXiv:1305.3976, Section 3.4, Steps 1a-3f
+ * (PAPER.md:574-697), on a periodic MAC grid in 2D or 3D,
+ * coupled to an elastic force-connection network through a
+ * 4-point delta kernel.
+ *
+ * Conventions common to every entry point
+ *   - Return value: IB_OK (0) or a negative IB_E* code; ib_last_error() returns a
+ *     thread-local message for the last failure.  No exception crosses the ABI.
+ *   - Host pointers: every pointer argument is a caller-owned HOST buffer.  Inputs
+ *     are copied during the call; outputs are written into caller-allocated
+ *     buffers of the documented size before the call returns.
+ *   - Field layout: a field of the N^d grid is N^d doubles, x fastest:
+ *     flat index i + N*(j + N*k).  u (x-velocity) lives at (i h, (j+1/2) h, (k+1/2) h),
+ *     v at ((i+1/2) h, j h, (k+1/2) h), w at ((i+1/2) h, (j+1/2) h, k h), p and psi at
+ *     cell centres ((i+1/2) h, ...) with h = H/N.
+ *   - Lagrangian arrays: X, U are [npts][dim] doubles (point-major), unwrapped
+ *     positions (only grid indices wrap periodically).
+ *   - Device memory and the CUDA stream are owned by the context (unless a stream
+ *     is passed in ib_options.stream); all device work of a call is ordered on that
+ *     stream.  Calls on one context are not thread-safe.
+ *   - With nranks > 1 (z-slab decomposition, not available in this build: returns
+ *     IB_EINVAL) field arrays would be the rank's local slab.
+ */
+#ifndef IBGM_H
+#define IBGM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IB_OK 0
+#define IB_EINVAL (-1)      /* invalid argument (dim, N, dt, rho, nu, chi, edge index ...) */
+#define IB_ESTATE (-2)      /* ib_step before ib_set_fields                                  */
+#define IB_ECUDA (-3)       /* a CUDA runtime call failed (message names it)                  */
+#define IB_ENCCL (-4)       /* reserved: NCCL failure (multi-GPU build)                       */
+#define IB_ENONFINITE (-5)  /* NaN/Inf detected in the state by ib_check_finite               */
+#define IB_EDOMAIN (-6)     /* reserved: IB point left the rank's slab + halo                 */
+#define IB_ENOMEM (-7)      /* device allocation failed                                       */
+
+#define IB_DELTA_COS4 0     /* phi(r) = (1 + cos(pi r/2))/4, |r| < 2: BASELINE.json configs */
+#define IB_DELTA_PESKIN4 1  /* the paper's kernel, eq. (discretedelta)    */
+
+typedef struct ib_ctx ib_ctx; /* opaque; owned by the library until ib_destroy */
+
+typedef struct {
+    int32_t dim; /* 2 or 3 */
+    int64_t n;   /* cells per side N; must have a divisor L in {2,3,4,6,8,12,16,24,32}
+                    with N/L <= 32 (line-solve segmentation), 8 <= N <= 1024           */
+    double H;    /* box side; must be 1 (the psi operator (1 - D_aa) is literal, R2)  */
+} ib_grid;
+
+typedef struct {
+    int32_t kernel;    /* IB_DELTA_COS4 (default) | IB_DELTA_PESKIN4                  */
+    double chi;        /* rotational correction weight chi in (0,1], default 0.6
+                                                                      */
+    int32_t advection; /* 1 (default): skew-symmetric advection;
+                          0: Stokes mode (closed-form tests)                            */
+    int32_t device;    /* CUDA ordinal, default 0                                       */
+    void* stream;      /* cudaStream_t to order all work on, or NULL (own stream)       */
+    int32_t rank;      /* z-slab rank (must be 0 in this build)                         */
+    int32_t nranks;    /* number of z-slabs (must be 1 in this build)                   */
+} ib_options;
+
+/* Fill *opt with the defaults listed above. */
+void ib_default_options(ib_options* opt);
+
+/* Create a context for the grid with kinematic viscosity nu = mu/rho, density rho
+ * and time step dt (epsilon = dt).  Allocates every device
+ * buffer and precomputes the line-solver factors.  *out receives the context.
+ * Errors: IB_EINVAL (dim not 2/3, N unsupported, H != 1, dt <= 0, rho <= 0, nu < 0,
+ * chi not in (0,1], nranks != 1), IB_ECUDA, IB_ENOMEM. */
+int ib_create(const ib_grid* grid, double nu, double rho, double dt, const ib_options* opt,
+              ib_ctx** out);
+
+/* Set the initial state: velocity u^0, v^0, (w^0: NULL in 2D) on the MAC faces and
+ * pressure p^{-1/2} (NULL -> 0); psi^{-1/2} = 0 and the step counter is reset to 0,
+ * which arms the start-up rules of PAPER.md:686-697.  Each array is N^d doubles. */
+int ib_set_fields(ib_ctx* ctx, const double* u, const double* v, const double* w,
+                  const double* p);
+
+/* Set the immersed boundary as a force-connection network:
+ * X[npts][dim] positions; edges[nedges][2] point indices; kappa[nedges] stiffness;
+ * rest[nedges] rest lengths (NULL -> 0); weight[npts] quadrature weights w_k used
+ * by spreading (NULL -> 1).  Edge e=(a,b) exerts F_a += kappa_e (X_b - X_a)
+ * (1 - rest_e/|X_b - X_a|) and the opposite on b (Step 2a).  A closed 2D fibre of
+ * PAPER.md:607-614 is kappa = sigma/h_s^2, rest = L h_s, weight = h_s.  Resets the
+ * step counter to 0.  Errors: IB_EINVAL (edge index out of range, npts < 0). */
+int ib_set_boundary(ib_ctx* ctx, int64_t npts, const double* X, int64_t nedges,
+                    const int64_t* edges, const double* kappa, const double* rest,
+                    const double* weight);
+
+/* BASELINE.json's ib_set_boundary(X, stiffness) for closed 2D fibres: n_fibers
+ * closed fibres, fibre f has pts_per_fiber[f] consecutive points in X, stiffness
+ * sigma, rest length 0; builds kappa = sigma/h_s^2, weight = h_s, h_s = 1/pts. */
+int ib_set_fibers(ib_ctx* ctx, int32_t n_fibers, const int64_t* pts_per_fiber,
+                  const double* X, double sigma);
+
+/* Advance nsteps time steps (Steps 1a-3f each).  All work is enqueued on the
+ * context's stream; the call returns after enqueueing (use ib_sync to wait).
+ * Errors: IB_ESTATE (no ib_set_fields yet), IB_ECUDA. */
+int ib_step(ib_ctx* ctx, int64_t nsteps);
+
+/* Block until all work enqueued on the context's stream has completed. */
+int ib_sync(ib_ctx* ctx);
+
+/* Copy the state to host buffers (any pointer may be NULL): u^n, v^n, w^n,
+ * p^{n-1/2}, psi^{n-1/2} (N^d each), X^n and U^{n-1} (the velocity interpolated in
+ * the last step) ([npts][dim]).  Synchronises the stream. */
+int ib_get_fields(ib_ctx* ctx, double* u, double* v, double* w, double* p, double* psi,
+                  double* X, double* U);
+
+/* Intermediates of the last step (any pointer may be NULL): the spread force
+ * f^{n+1/2} per component (N^d each), the stored advection N(u^n) per component,
+ * the Lagrangian force F^{n+1/2} and X^{n+1/2} ([npts][dim]).  F is the force of
+ * Step 2a BEFORE the quadrature weight is applied. */
+int ib_get_aux(ib_ctx* ctx, double* fu, double* fv, double* fw, double* nu, double* nv,
+               double* nw, double* F, double* Xh);
+
+/* Stand-alone batched cyclic tridiagonal solve on the GPU (the line solver of
+ * PAPER.md:946-1276 used by every step): for every grid line of the N^d array `d`
+ * along `axis` (0 = x, 1 = y, 2 = z) solve  c x_{i-1} + a x_i + c x_{i+1} = d_i
+ * (indices mod N) with a = 1 + 2 kappa, c = -kappa, and write x (N^d, may alias d).
+ * Uses the same kernels, segmentation and mean correction as ib_step.  Host buffers.
+ * Errors: IB_EINVAL (kappa < 0, axis >= dim). */
+int ib_line_solve(ib_ctx* ctx, int32_t axis, double kappa, const double* d, double* x);
+
+/* Device-side finiteness check of u, p and X; IB_ENONFINITE if any NaN/Inf. */
+int ib_check_finite(ib_ctx* ctx);
+
+/* Number of kernels this library launched since the context was created, and the
+ * number of completed steps. */
+int ib_get_stats(ib_ctx* ctx, int64_t* kernel_launches, int64_t* steps_done);
+
+/* Phases of one step, for ib_get_phase_times (one kernel or memset each). */
+#define IB_PH_INTERP 0   /* Steps 1a-1c: interpolate U^n, evolve X          */
+#define IB_PH_FORCE 1    /* Step 2a: force-connection forces               */
+#define IB_PH_ZERO_F 2   /* clear f before spreading                        */
+#define IB_PH_SPREAD 3   /* Step 2b: spread F to f                          */
+#define IB_PH_S1 4       /* Steps 3a-3c: p*, explicit momentum, x sweep     */
+#define IB_PH_VISC_Y 5   /* Step 3d: y sweep                                */
+#define IB_PH_VISC_Z 6   /* z sweep (3D)                                    */
+#define IB_PH_DIV 7      /* Step 3e RHS and the explicit part of Step 3f    */
+#define IB_PH_PSI_Z 8    /* psi factor (1 - D_zz) (3D)                       */
+#define IB_PH_PSI_Y 9    /* psi factor (1 - D_yy)                            */
+#define IB_PH_PSI_X 10   /* psi factor (1 - D_xx) + Step 3f p = q + psi     */
+#define IB_NPHASES 11
+
+/* Turn per-phase CUDA-event timing on (1) or off (0).  While on, ib_step records an
+ * event pair around every phase on the context's stream and synchronises at the end
+ * of each ib_step call to accumulate the elapsed times; turning it on resets them. */
+int ib_set_profiling(ib_ctx* ctx, int32_t on);
+
+/* Accumulated milliseconds and launch counts per phase (arrays of IB_NPHASES). */
+int ib_get_phase_times(ib_ctx* ctx, double* ms, int64_t* count);
+
+/* Release every device buffer, the stream (if owned) and the context. */
+int ib_destroy(ib_ctx* ctx);
+
+/* Thread-local message describing the last non-zero return of this thread. */
+const char* ib_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IBGM_H */

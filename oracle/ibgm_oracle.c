@@ -281,6 +281,13 @@ static void solve_axis(const orc_grid* g, double* q, int ax, double c, double a,
     free(line); free(sol); free(ws);
 }
 
+/* Exported: solve every line of the N^dim array q along `axis`, in place. */
+void orc_solve_axis(int dim, long n, int axis, double c, double a, double b, double* q)
+{
+    orc_grid g = {dim, n, 1.0 / (double)n};
+    solve_axis(&g, q, axis, c, a, b);
+}
+
 /* ------------------------------------------------------------------------- */
 /* Exported single-operator entry points (used by the oracle's pin tests).    */
 /* ------------------------------------------------------------------------- */

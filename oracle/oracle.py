@@ -44,6 +44,8 @@ def lib():
         L.orc_phi.argtypes = [ctypes.c_int, ctypes.c_double]
         L.orc_cyclic_solve.argtypes = [ctypes.c_long, ctypes.c_double, ctypes.c_double,
                                        ctypes.c_double, _dp, _dp]
+        L.orc_solve_axis.argtypes = [ctypes.c_int, ctypes.c_long, ctypes.c_int, ctypes.c_double,
+                                     ctypes.c_double, ctypes.c_double, _dp]
         L.orc_op_d2.argtypes = [ctypes.c_int, ctypes.c_long, ctypes.c_int, _dp, _dp]
         L.orc_op_grad.argtypes = [ctypes.c_int, ctypes.c_long, ctypes.c_int, _dp, _dp]
         L.orc_op_div.argtypes = [ctypes.c_int, ctypes.c_long, _dp, _dp, _dp, _dp]
@@ -94,6 +96,13 @@ def cyclic_solve(c: float, a: float, b: float, d) -> np.ndarray:
     x = np.empty_like(d)
     lib().orc_cyclic_solve(d.size, c, a, b, _p(d), _p(x))
     return x
+
+
+def solve_axis(q, axis: int, c: float, a: float, b: float) -> np.ndarray:
+    """Cyclic solve of every grid line of q along `axis` (0 = x, the last array axis)."""
+    q = _c(q).copy()
+    lib().orc_solve_axis(q.ndim, q.shape[0], axis, c, a, b, _p(q))
+    return q
 
 
 def _shape(dim, n):

@@ -1,0 +1,89 @@
+// Internal declarations shared by the CUDA translation units of libibgm.so.
+// Product code; shares nothing with oracle/.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/ibgm.h"
+
+namespace ibgm {
+
+constexpr int kMaxSeg = 32;   // max segments P per line (reduced Schur system size)
+constexpr int kMaxL = 32;     // max segment length L
+
+// Constant-coefficient cyclic tridiagonal system  c x_{i-1} + a x_i + b x_{i+1} = d_i
+// solved by the paper's Schur-complement splitting applied
+// inside a thread block: each line of N = P*L unknowns is cut into P parts; part p
+// is one interface unknown y_p = x_{pL} followed by an interior block of m = L-1
+// unknowns (the B_p of eq. BlockSchurSystem).  Everything below is line-independent
+// and precomputed once on the host in long double (PAPER.md:1260-1262:
+// "S and B^{-1}E can be precomputed").
+struct LineCoef {
+    double c, a, b;           // sub, diag, super
+    double inv_rowsum;        // 1/(a+b+c): mean(x) = mean(d)/(a+b+c) for circulant A
+    int L, P, N, mean_fix;
+    double inv[kMaxL];        // Thomas: 1/den_i of B (i = 0..m-1)
+    double cp[kMaxL];         // Thomas: b/den_i
+    double g[kMaxL];          // B^{-1} e_1   (first column of B^{-1})
+    double h[kMaxL];          // B^{-1} e_m   (last column of B^{-1})
+    double sinv[kMaxSeg * kMaxSeg];  // dense inverse of the P x P periodic Schur matrix S
+};
+
+enum SysId { SYS_VISC = 0, SYS_PSI = 1, SYS_USER = 2, SYS_COUNT = 3 };
+
+struct Ctx {
+    int dim;
+    int64_t n, ncell;
+    double h, mu, rho, dt, chi;
+    int kernel, advection, device;
+    cudaStream_t stream;
+    bool own_stream;
+    int L, P, R;                      // line segmentation: N = P*L, R lines per block
+    // Eulerian state (device), each ncell doubles
+    double* u[3];                     // u^n
+    double* st[3];                    // stage buffer: u**, u***, u^{n+1}
+    double* nadv[3];                  // N(u^n), written this step
+    double* nprev[3];                 // N(u^{n-1})
+    double* f[3];                     // spread force f^{n+1/2}
+    double* p;                        // p^{n-1/2}  (holds q = p - chi mu D.u_bar mid-step)
+    double* psi;                      // psi^{n-1/2} (holds the psi RHS / factors mid-step)
+    LineCoef* coef;                   // device copies, SYS_COUNT entries
+    LineCoef hcoef[SYS_COUNT];        // host copies
+    // Lagrangian state (device)
+    int64_t npts, nedges;
+    double *X, *Xh, *Uprev, *F, *wgt;   // Uprev: U interpolated in the last step
+    int32_t* csr_ptr;                 // [npts+1]
+    int32_t* csr_nbr;                 // [2*nedges]
+    double* csr_kappa;                // [2*nedges]
+    double* csr_rest;                 // [2*nedges]
+    int has_rest;
+    int64_t step;                     // steps completed since set_fields/set_boundary
+    bool fields_set;
+    int64_t launches;
+    int* d_flag;                      // device flag for finiteness checks
+    // per-phase profiling (ib_set_profiling)
+    int profiling;
+    cudaEvent_t ev[IB_NPHASES][2];
+    bool ev_made;
+    double ph_ms[IB_NPHASES];
+    int64_t ph_cnt[IB_NPHASES];
+    bool ph_pending[IB_NPHASES];
+};
+
+// host-side precompute (api.cu)
+void make_line_coef(LineCoef* C, int64_t N, int L, double c, double a, double b, int mean_fix);
+
+// launchers (fluid.cu)
+cudaError_t launch_s1_x(Ctx* s, int first_step);             // RHS + AB2 + x-sweep (Steps 3a-3c)
+cudaError_t launch_visc_sweep(Ctx* s, int axis);             // y or z Douglas sweep (Step 3d)
+cudaError_t launch_div(Ctx* s);                              // r = -(rho/dt) D.u^{n+1}; q = p - chi mu D.u_bar
+cudaError_t launch_psi_sweep(Ctx* s, int axis, int last);    // psi factor along axis; last: p = q + psi
+cudaError_t launch_line_solve(Ctx* s, int axis, int sys, double* data);  // stand-alone solve
+// IB (ib.cu)
+cudaError_t launch_interp_evolve(Ctx* s, int first_step);    // Steps 1a-1c
+cudaError_t launch_force(Ctx* s);                            // Step 2a
+cudaError_t launch_spread(Ctx* s);                           // Step 2b
+cudaError_t launch_check_finite(Ctx* s);
+
+}  // namespace ibgm

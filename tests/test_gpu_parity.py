@@ -1,0 +1,248 @@
+"""GPU parity: the CUDA path (called through the C-ABI, include/ibgm.h) against the
+CPU oracle (oracle/), element by element on the same seeded inputs.
+
+Bars (BASELINE.json north_star): rel L_inf <= 1e-9 on u (each component), p and X
+after 10 steps; line solves on identical right-hand sides <= 1e-12.  rel L_inf =
+max|gpu - oracle| / max|oracle|.
+"""
+import numpy as np
+import pytest
+
+from conftest import stag_coords
+
+pytestmark = pytest.mark.gpu
+
+RNG = np.random.default_rng(20260)
+
+
+def _rel(a, b):
+    den = np.abs(b).max()
+    return float(np.abs(a - b).max() / (den if den > 0 else 1.0))
+
+
+def _ctx(**kw):
+    from paper_1305_3976_b200 import ibgm
+    return ibgm.Context(**kw)
+
+
+def _oracle_for(pr, **kw):
+    from oracle import oracle as O
+    o = O.Oracle(pr.dim, pr.n, pr.mu, pr.rho, pr.dt, chi=pr.chi, kernel=pr.kernel, **kw)
+    o.set_fields(*pr.u, p=pr.p) if pr.dim == 3 else o.set_fields(pr.u[0], pr.u[1], None, pr.p)
+    if pr.X is not None:
+        o.set_boundary(pr.X, pr.edges, pr.kappa, rest=pr.rest, weight=pr.weight)
+    return o
+
+
+def _gpu_for(pr, **kw):
+    from paper_1305_3976_b200 import ibgm
+    return ibgm.from_problem(pr, **kw)
+
+
+# ------------------------------------------------------------------ line solves
+@pytest.mark.parametrize("dim,n", [(2, 32), (2, 20), (2, 12), (2, 256), (2, 1024), (3, 16), (3, 20), (3, 128)])
+@pytest.mark.parametrize("which", ["visc", "psi"])
+def test_line_solve_parity(dim, n, which):
+    """Batched cyclic solves along every axis vs the oracle's long-double
+    Thomas + Sherman-Morrison, identical right-hand sides: <= 1e-12 (north_star)."""
+    from oracle import oracle as O
+    ctx = _ctx(dim=dim, n=n, nu=0.01, rho=1.0, dt=1e-3)
+    kap = 0.0524 if which == "visc" else float(n) ** 2
+    d = RNG.standard_normal((n,) * dim)
+    for axis in range(dim):
+        x = ctx.line_solve(axis, kap, d)
+        ref = O.solve_axis(d, axis, -kap, 1 + 2 * kap, -kap)
+        assert _rel(x, ref) <= 1e-12, (axis, _rel(x, ref))
+    ctx.close()
+
+
+def test_line_solve_full_size_sampled_3d_384():
+    """Config-4 size (384^3, the bench's largest launch shape): psi and viscous systems,
+    every axis, checked on 64 sampled lines per axis against the oracle."""
+    from oracle import oracle as O
+    n = 384
+    ctx = _ctx(dim=3, n=n, nu=0.005, rho=1.0, dt=5e-5)
+    d = RNG.standard_normal((n, n, n))
+    for kap in (0.0184, float(n) ** 2):
+        for axis in range(3):
+            x = ctx.line_solve(axis, kap, d)
+            for _ in range(64):
+                a, b = RNG.integers(0, n, 2)
+                if axis == 0:
+                    line, got = d[a, b, :], x[a, b, :]
+                elif axis == 1:
+                    line, got = d[a, :, b], x[a, :, b]
+                else:
+                    line, got = d[:, a, b], x[:, a, b]
+                ref = O.cyclic_solve(-kap, 1 + 2 * kap, -kap, line)
+                assert _rel(got, ref) <= 1e-12
+    ctx.close()
+
+
+# ------------------------------------------------------------------ one step, per stage
+@pytest.mark.parametrize("cfg,over", [(0, {}), (1, dict(n=64, pts=256)), (3, dict(n=32, nodes=2000)),
+                                      (4, dict(n=48, nodes=1500))])
+def test_one_step_stage_parity(cfg, over):
+    """After one step: X^{n+1/2}, F^{n+1/2}, spread f, N(u^n), then u, p, psi, X."""
+    from paper_1305_3976_b200 import inputs
+    pr = inputs.config(cfg, **over)
+    o = _oracle_for(pr)
+    g = _gpu_for(pr)
+    o.step(1)
+    g.step(1)
+    ao, ag = o.aux(), g.aux()
+    assert _rel(ag["Xh"], ao["Xh"]) <= 1e-14
+    assert _rel(ag["F"], ao["F"]) <= 1e-12
+    for c in range(pr.dim):
+        assert _rel(ag["f"][c], ao["f"][c]) <= 1e-12, ("f", c)
+        if np.abs(ao["nadv"][c]).max() > 0:
+            assert _rel(ag["nadv"][c], ao["nadv"][c]) <= 1e-12, ("N", c)
+    fo, fg = o.fields(), g.fields()
+    for c in range(pr.dim):
+        assert _rel(fg["u"][c], fo["u"][c]) <= 1e-11, ("u", c)
+    assert _rel(fg["p"], fo["p"]) <= 1e-11
+    assert _rel(fg["psi"], fo["psi"]) <= 1e-11
+    assert _rel(fg["X"], fo["X"]) <= 1e-14
+    g.close()
+
+
+# ------------------------------------------------------------------ 10 steps, configs
+@pytest.mark.parametrize("cfg,over", [(0, {}), (1, {}), (2, {}), (3, {}), (4, dict(n=96, nodes=4000)),
+                                      (2, dict(n=128, pts=256, kernel=1))])
+def test_ten_step_parity(cfg, over):
+    """End-to-end bar of the north_star: rel L_inf <= 1e-9 on u, p and X after 10 steps.
+    Configs 0-3 at full size; config 4 at reduced N here (full size sampled below)."""
+    from paper_1305_3976_b200 import inputs
+    pr = inputs.config(cfg, **over)
+    o = _oracle_for(pr)
+    g = _gpu_for(pr)
+    o.step(10)
+    g.step(10)
+    fo, fg = o.fields(), g.fields()
+    for c in range(pr.dim):
+        assert _rel(fg["u"][c], fo["u"][c]) <= 1e-9, ("u", c, _rel(fg["u"][c], fo["u"][c]))
+    assert _rel(fg["p"], fo["p"]) <= 1e-9, _rel(fg["p"], fo["p"])
+    assert _rel(fg["X"], fo["X"]) <= 1e-9
+    assert _rel(fg["U"], fo["U"]) <= 1e-9
+    g.check_finite()
+    g.close()
+
+
+@pytest.mark.slow
+def test_config4_full_size_one_step():
+    """Config 4 at full size (384^3, 8 x 100k-node shells): one step, every field
+    against the oracle (about two minutes of oracle time)."""
+    from paper_1305_3976_b200 import inputs
+    pr = inputs.config(4)
+    g = _gpu_for(pr)
+    g.step(1)
+    fg = g.fields()
+    g.close()
+    o = _oracle_for(pr)
+    o.step(1)
+    fo = o.fields()
+    for c in range(3):
+        assert _rel(fg["u"][c], fo["u"][c]) <= 1e-9
+    assert _rel(fg["p"], fo["p"]) <= 1e-9
+    assert _rel(fg["X"], fo["X"]) <= 1e-9
+
+
+# ------------------------------------------------------------------ closed forms on the GPU
+@pytest.mark.parametrize("dim", [2, 3])
+def test_gpu_stokes_taylor_green_closed_form(dim):
+    """Independent of the oracle: solenoidal mode, Stokes mode, G = 1 - 2a sum(lam)/prod(1+a lam)."""
+    n = 32 if dim == 2 else 16
+    mu, rho, dt = 0.05, 1.0, 2e-3
+    k = np.array([2, 1, 3])[:dim]
+    h = 1.0 / n
+    lam = 4 * np.sin(np.pi * k * h) ** 2 / h ** 2
+    s = np.sin(np.pi * k * h)
+    uhat = np.array([s[1], -s[0]]) if dim == 2 else np.cross(s, np.array([0.3, -0.5, 0.8]))
+    u0 = []
+    for c in range(dim):
+        co = stag_coords(dim, n, c)
+        ph = sum(2 * np.pi * k[a] * co[a] for a in range(dim))
+        u0.append(uhat[c] * np.cos(ph))
+    ctx = _ctx(dim=dim, n=n, nu=mu / rho, rho=rho, dt=dt, advection=False)
+    ctx.set_fields(*u0) if dim == 3 else ctx.set_fields(u0[0], u0[1])
+    ctx.step(10)
+    fg = ctx.fields()
+    a = mu * dt / (2 * rho)
+    G = 1 - 2 * a * lam.sum() / np.prod(1 + a * lam)
+    scale = max(np.abs(x).max() for x in u0)
+    for c in range(dim):
+        assert np.abs(fg["u"][c] - G ** 10 * u0[c]).max() <= 1e-13 * scale
+    assert np.abs(fg["p"]).max() < 1e-9 and np.abs(fg["psi"]).max() < 1e-9
+    ctx.close()
+
+
+# ------------------------------------------------------------------ edge cases
+def test_no_immersed_boundary_and_rest_lengths():
+    """npts = 0 (pure fluid) and a fibre with non-zero rest length (L != 0 branch)."""
+    from paper_1305_3976_b200 import inputs
+    pr = inputs.config(1, n=32, pts=64)
+    pr.X = None
+    o = _oracle_for(pr)
+    g = _gpu_for(pr)
+    o.step(5); g.step(5)
+    fo, fg = o.fields(), g.fields()
+    assert _rel(fg["u"][0], fo["u"][0]) <= 1e-10 and _rel(fg["p"], fo["p"]) <= 1e-10
+    g.close()
+    pr = inputs.config(0)
+    pr.rest = np.full(pr.edges.shape[0], 0.5 / 128)
+    o = _oracle_for(pr)
+    g = _gpu_for(pr)
+    o.step(5); g.step(5)
+    fo, fg = o.fields(), g.fields()
+    assert _rel(fg["X"], fo["X"]) <= 1e-10 and _rel(fg["u"][1], fo["u"][1]) <= 1e-10
+    g.close()
+
+
+def test_points_outside_unit_box_wrap():
+    """Unwrapped positions beyond [0,1) use periodic images (R7)."""
+    from paper_1305_3976_b200 import inputs
+    pr = inputs.config(0)
+    pr.X = pr.X + np.array([1.0, -2.0])
+    o = _oracle_for(pr)
+    g = _gpu_for(pr)
+    o.step(3); g.step(3)
+    fo, fg = o.fields(), g.fields()
+    assert _rel(fg["u"][0], fo["u"][0]) <= 1e-10 and _rel(fg["X"], fo["X"]) <= 1e-12
+    g.close()
+
+
+def test_set_fibers_equals_explicit_edges():
+    """BASELINE's ib_set_boundary(X, stiffness) form == the explicit edge form."""
+    from paper_1305_3976_b200 import inputs
+    pr = inputs.config(2, n=64, pts=128)
+    g1 = _gpu_for(pr)
+    from paper_1305_3976_b200 import ibgm
+    g2 = ibgm.Context(2, pr.n, pr.mu / pr.rho, pr.rho, pr.dt)
+    g2.set_fields(pr.u[0], pr.u[1], None, pr.p)
+    g2.set_fibers([128] * 4, pr.X, 1.0)
+    g1.step(4); g2.step(4)
+    a, b = g1.fields(), g2.fields()
+    assert _rel(a["X"], b["X"]) <= 1e-15 and _rel(a["u"][0], b["u"][0]) <= 1e-14
+    g1.close(); g2.close()
+
+
+def test_step_before_set_fields_is_an_error():
+    from paper_1305_3976_b200 import ibgm
+    ctx = ibgm.Context(2, 32, 0.01, 1.0, 1e-3)
+    with pytest.raises(ibgm.IBGMError) as e:
+        ctx.step(1)
+    assert e.value.code == -2
+    ctx.close()
+
+
+def test_nonfinite_is_detected():
+    from paper_1305_3976_b200 import ibgm
+    n = 16
+    ctx = ibgm.Context(2, n, 0.01, 1.0, 1e-3)
+    u = np.zeros((n, n)); u[3, 4] = np.nan
+    ctx.set_fields(u, np.zeros((n, n)))
+    ctx.step(1)
+    with pytest.raises(ibgm.IBGMError) as e:
+        ctx.check_finite()
+    assert e.value.code == -5
+    ctx.close()
