@@ -191,7 +191,11 @@ def main():
     from paper_1305_3976_b200 import ibgm, inputs
     pr = inputs.config(args.config)
     dim, n = pr.dim, pr.n
-    stream = torch.cuda.current_stream()
+    # a dedicated (non-default) stream: the library enqueues every kernel on it and the
+    # timing events below are recorded on the same stream
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    assert stream.cuda_stream != 0
     ctx = ibgm.from_problem(pr, device=local, stream=stream.cuda_stream)
 
     def barrier():

@@ -117,7 +117,8 @@ int ib_get_fields(ib_ctx* ctx, double* u, double* v, double* w, double* p, doubl
                   double* X, double* U);
 
 /* Intermediates of the last step (any pointer may be NULL): the spread force
- * f^{n+1/2} per component (N^d each), the stored advection N(u^n) per component,
+ * f^{n+1/2} per component (N^d each; requires ib_set_debug bit 0 before the step,
+ * else IB_ESTATE), the stored advection N(u^n) per component,
  * the Lagrangian force F^{n+1/2} and X^{n+1/2} ([npts][dim]).  F is the force of
  * Step 2a BEFORE the quadrature weight is applied. */
 int ib_get_aux(ib_ctx* ctx, double* fu, double* fv, double* fw, double* nu, double* nv,
@@ -138,19 +139,23 @@ int ib_check_finite(ib_ctx* ctx);
  * number of completed steps. */
 int ib_get_stats(ib_ctx* ctx, int64_t* kernel_launches, int64_t* steps_done);
 
-/* Phases of one step, for ib_get_phase_times (one kernel or memset each). */
-#define IB_PH_INTERP 0   /* Steps 1a-1c: interpolate U^n, evolve X          */
-#define IB_PH_FORCE 1    /* Step 2a: force-connection forces               */
-#define IB_PH_ZERO_F 2   /* clear f before spreading                        */
-#define IB_PH_SPREAD 3   /* Step 2b: spread F to f                          */
-#define IB_PH_S1 4       /* Steps 3a-3c: p*, explicit momentum, x sweep     */
-#define IB_PH_VISC_Y 5   /* Step 3d: y sweep                                */
-#define IB_PH_VISC_Z 6   /* z sweep (3D)                                    */
-#define IB_PH_DIV 7      /* Step 3e RHS and the explicit part of Step 3f    */
-#define IB_PH_PSI_Z 8    /* psi factor (1 - D_zz) (3D)                       */
-#define IB_PH_PSI_Y 9    /* psi factor (1 - D_yy)                            */
-#define IB_PH_PSI_X 10   /* psi factor (1 - D_xx) + Step 3f p = q + psi     */
-#define IB_NPHASES 11
+/* Phases of one step, for ib_get_phase_times (one kernel launch each). */
+#define IB_PH_INTERP 0   /* Steps 1a-1c: interpolate U^n, evolve X                         */
+#define IB_PH_FORCE 1    /* Step 2a: force-connection forces                              */
+#define IB_PH_SPREAD 2   /* Step 2b: spread F into the momentum history                    */
+#define IB_PH_S1 3       /* Steps 3a-3c: p*, explicit momentum, x sweep                    */
+#define IB_PH_SWEEP_Y 4  /* Step 3d: y sweep (2D: the last sweep, u^{n+1} = u^n + d)       */
+#define IB_PH_SWEEP_Z 5  /* z sweep, u^{n+1} = u^n + d (3D)                                */
+#define IB_PH_DIVPSI 6   /* Step 3e RHS D.u^{n+1} + first psi factor + explicit part of 3f */
+#define IB_PH_PSI_Y 7    /* psi factor (1 - D_yy) (3D)                                      */
+#define IB_PH_PSI_X 8    /* psi factor (1 - D_xx) + Step 3f p = q + psi, p* = p + psi      */
+#define IB_PH_CLEAR 9    /* history clear at n = 0 and debug clears                        */
+#define IB_NPHASES 10
+
+/* Debug flags: bit 0 keeps the spread force f^{n+1/2} as a separate field so that
+ * ib_get_aux can return it (costs one extra atomic per spread contribution and a
+ * clear per step).  Off by default. */
+int ib_set_debug(ib_ctx* ctx, int32_t flags);
 
 /* Turn per-phase CUDA-event timing on (1) or off (0).  While on, ib_step records an
  * event pair around every phase on the context's stream and synchronises at the end

@@ -48,9 +48,10 @@ namespace ibgm {
 // and the interface equations give the periodic P x P Schur matrix
 //   S_pp = a - b c (h_m + g_1),  S_{p,p-1} = -c^2 g_m,  S_{p,p+1} = -b^2 h_1
 // (PAPER.md:1192-1219 specialised to constant-coefficient lines).
-void make_line_coef(LineCoef* C, int64_t N, int L, double c_, double a_, double b_, int mean_fix)
+void make_line_coef(LineCoef* C, SchurInv* SI, int64_t N, int L, double c_, double a_, double b_, int mean_fix)
 {
     memset(C, 0, sizeof(*C));
+    memset(SI, 0, sizeof(*SI));
     const long double c = c_, a = a_, b = b_;
     const int m = L - 1;
     const int P = (int)(N / L);
@@ -80,10 +81,15 @@ void make_line_coef(LineCoef* C, int64_t N, int L, double c_, double a_, double 
     em[m - 1] = 1.0L;
     solveB(e1, g);
     solveB(em, h);
+    long double gs = 0.0L, hs = 0.0L;
     for (int i = 0; i < m; ++i) {
         C->g[i] = (double)g[i];
         C->h[i] = (double)h[i];
+        gs += g[i];
+        hs += h[i];
     }
+    C->gsum = (double)gs;
+    C->hsum = (double)hs;
     const long double s0 = a - b * c * (h[m - 1] + g[0]);
     const long double sm = -c * c * g[m - 1];
     const long double sp = -b * b * h[0];
@@ -119,19 +125,23 @@ void make_line_coef(LineCoef* C, int64_t N, int L, double c_, double a_, double 
             }
         }
     }
-    for (int i = 0; i < P * P; ++i) C->sinv[i] = (double)I[i];
+    for (int i = 0; i < P * P; ++i) SI->sinv[i] = (double)I[i];
+    for (int q = 0; q < P; ++q) {
+        long double cs = 0.0L;
+        for (int p = 0; p < P; ++p) cs += I[(size_t)p * P + q];
+        SI->colsum[q] = (double)cs;
+    }
 }
 
 }  // namespace ibgm
 
-static bool choose_segmentation(int64_t n, int* L, int* P, int* R)
+static bool choose_segmentation(int64_t n, int* L, int* P)
 {
     static const int cands[] = {8, 12, 16, 24, 32, 6, 4, 3, 2};
     for (int c : cands) {
         if (n % c == 0 && n / c <= kMaxSeg) {
             *L = c;
             *P = (int)(n / c);
-            *R = (*P <= 16) ? 32 : 16;
             return true;
         }
     }
@@ -177,8 +187,8 @@ int ib_create(const ib_grid* grid, double nu, double rho, double dt, const ib_op
     if (!(o.chi > 0 && o.chi <= 1)) return fail(IB_EINVAL, "chi must be in (0, 1]");
     if (o.nranks != 1 || o.rank != 0) return fail(IB_EINVAL, "this build runs one rank per process (nranks = 1)");
     if (o.kernel != IB_DELTA_COS4 && o.kernel != IB_DELTA_PESKIN4) return fail(IB_EINVAL, "unknown delta kernel");
-    int L, P, R;
-    if (!choose_segmentation(grid->n, &L, &P, &R))
+    int L, P;
+    if (!choose_segmentation(grid->n, &L, &P))
         return fail(IB_EINVAL, "N = %lld has no divisor L in {2,3,4,6,8,12,16,24,32} with N/L <= 32",
                     (long long)grid->n);
 
@@ -196,7 +206,7 @@ int ib_create(const ib_grid* grid, double nu, double rho, double dt, const ib_op
     s->kernel = o.kernel;
     s->advection = o.advection;
     s->device = o.device;
-    s->L = L; s->P = P; s->R = R;
+    s->L = L; s->P = P;
     *out = c;
 
     CKC(cudaSetDevice(o.device));
@@ -213,27 +223,27 @@ int ib_create(const ib_grid* grid, double nu, double rho, double dt, const ib_op
         CKC(cudaMalloc(&s->st[q], fb));
         CKC(cudaMalloc(&s->nadv[q], fb));
         CKC(cudaMalloc(&s->nprev[q], fb));
-        CKC(cudaMalloc(&s->f[q], fb));
         CKC(cudaMemsetAsync(s->u[q], 0, fb, s->stream));
         CKC(cudaMemsetAsync(s->st[q], 0, fb, s->stream));
         CKC(cudaMemsetAsync(s->nadv[q], 0, fb, s->stream));
         CKC(cudaMemsetAsync(s->nprev[q], 0, fb, s->stream));
-        CKC(cudaMemsetAsync(s->f[q], 0, fb, s->stream));
     }
     CKC(cudaMalloc(&s->p, fb));
-    CKC(cudaMalloc(&s->psi, fb));
+    CKC(cudaMalloc(&s->pstar, fb));
+    CKC(cudaMalloc(&s->tmp, fb));
     CKC(cudaMemsetAsync(s->p, 0, fb, s->stream));
-    CKC(cudaMemsetAsync(s->psi, 0, fb, s->stream));
+    CKC(cudaMemsetAsync(s->pstar, 0, fb, s->stream));
     CKC(cudaMalloc(&s->d_flag, sizeof(int)));
-    CKC(cudaMalloc(&s->coef, sizeof(LineCoef) * SYS_COUNT));
+    CKC(cudaMalloc(&s->sinv, sizeof(SchurInv) * SYS_COUNT));
+    SchurInv hs[SYS_COUNT];
     // viscous Douglas sweeps: (1 - kap delta) with kap = mu dt / (2 rho h^2)
     const double kv = s->mu * dt / (2.0 * rho * s->h * s->h);
-    make_line_coef(&s->hcoef[SYS_VISC], s->n, L, -kv, 1.0 + 2.0 * kv, -kv, 1);
+    make_line_coef(&s->hcoef[SYS_VISC], &hs[SYS_VISC], s->n, L, -kv, 1.0 + 2.0 * kv, -kv, 1);
     // psi factors: (1 - D_aa) with D_aa = delta / h^2 (R2)
     const double kp = 1.0 / (s->h * s->h);
-    make_line_coef(&s->hcoef[SYS_PSI], s->n, L, -kp, 1.0 + 2.0 * kp, -kp, 1);
-    make_line_coef(&s->hcoef[SYS_USER], s->n, L, -kv, 1.0 + 2.0 * kv, -kv, 1);
-    CKC(cudaMemcpyAsync(s->coef, s->hcoef, sizeof(LineCoef) * SYS_COUNT, cudaMemcpyHostToDevice, s->stream));
+    make_line_coef(&s->hcoef[SYS_PSI], &hs[SYS_PSI], s->n, L, -kp, 1.0 + 2.0 * kp, -kp, 1);
+    make_line_coef(&s->hcoef[SYS_USER], &hs[SYS_USER], s->n, L, -kv, 1.0 + 2.0 * kv, -kv, 1);
+    CKC(cudaMemcpyAsync(s->sinv, hs, sizeof(SchurInv) * SYS_COUNT, cudaMemcpyHostToDevice, s->stream));
     CKC(cudaStreamSynchronize(s->stream));
     return IB_OK;
 }
@@ -248,9 +258,14 @@ int ib_set_fields(ib_ctx* c, const double* u, const double* v, const double* w, 
         CKC(cudaMemcpyAsync(s->u[q], in[q], fb, cudaMemcpyHostToDevice, s->stream));
         CKC(cudaMemsetAsync(s->nprev[q], 0, fb, s->stream));
     }
-    if (p) CKC(cudaMemcpyAsync(s->p, p, fb, cudaMemcpyHostToDevice, s->stream));
-    else CKC(cudaMemsetAsync(s->p, 0, fb, s->stream));
-    CKC(cudaMemsetAsync(s->psi, 0, fb, s->stream));
+    // p^{-1/2} = p (or 0), psi^{-1/2} = 0, so p* = p (R5)
+    if (p) {
+        CKC(cudaMemcpyAsync(s->p, p, fb, cudaMemcpyHostToDevice, s->stream));
+        CKC(cudaMemcpyAsync(s->pstar, p, fb, cudaMemcpyHostToDevice, s->stream));
+    } else {
+        CKC(cudaMemsetAsync(s->p, 0, fb, s->stream));
+        CKC(cudaMemsetAsync(s->pstar, 0, fb, s->stream));
+    }
     CKC(cudaStreamSynchronize(s->stream));
     s->step = 0;
     s->fields_set = true;
@@ -346,11 +361,11 @@ int ib_set_fibers(ib_ctx* c, int32_t n_fibers, const int64_t* pts_per_fiber, con
     return ib_set_boundary(c, npts, X, npts, edges.data(), kap.data(), nullptr, w.data());
 }
 
-static cudaError_t zero_f(Ctx* s)
+static cudaError_t clear3(Ctx* s, double* const* f)
 {
     const size_t fb = (size_t)s->ncell * sizeof(double);
     for (int q = 0; q < s->dim; ++q) {
-        cudaError_t e = cudaMemsetAsync(s->f[q], 0, fb, s->stream);
+        cudaError_t e = cudaMemsetAsync(f[q], 0, fb, s->stream);
         if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
@@ -373,26 +388,32 @@ int ib_step(ib_ctx* c, int64_t nsteps)
     Ctx* s = &c->s;
     if (!s->fields_set) return fail(IB_ESTATE, "ib_step before ib_set_fields");
     if (nsteps < 0) return fail(IB_EINVAL, "nsteps < 0");
+    const int d = s->dim;
     for (int64_t t = 0; t < nsteps; ++t) {
         const int first = (s->step == 0);
+        // n = 0: no N(u^{-1}); the history G starts as 0 + (2/rho) f
+        if (first) PHASE(IB_PH_CLEAR, clear3(s, s->nprev));
+        if (s->debug_keep_f && s->npts > 0) PHASE(IB_PH_CLEAR, clear3(s, s->f));
         if (s->npts > 0) {
             // Step 1 (interpolate, evolve) and Step 2 (force, spread)
             PHASE(IB_PH_INTERP, launch_interp_evolve(s, first));
             PHASE(IB_PH_FORCE, launch_force(s));
-            PHASE(IB_PH_ZERO_F, zero_f(s));
             PHASE(IB_PH_SPREAD, launch_spread(s));
         }
-        // Step 3a-3c: p*, explicit momentum, x sweep
+        // Steps 3a-3c: p*, explicit momentum, x sweep
         PHASE(IB_PH_S1, launch_s1_x(s, first));
-        // Step 3d (+ z): remaining Douglas sweeps
-        PHASE(IB_PH_VISC_Y, launch_visc_sweep(s, 1));
-        if (s->dim == 3) PHASE(IB_PH_VISC_Z, launch_visc_sweep(s, 2));
-        // Step 3e: psi right-hand side and factors; Step 3f fused into the last factor
-        PHASE(IB_PH_DIV, launch_div(s));
-        if (s->dim == 3) PHASE(IB_PH_PSI_Z, launch_psi_sweep(s, 2, 0));
-        PHASE(IB_PH_PSI_Y, launch_psi_sweep(s, 1, 0));
-        PHASE(IB_PH_PSI_X, launch_psi_sweep(s, 0, 1));
-        for (int q = 0; q < s->dim; ++q) {
+        // Step 3d: the remaining Douglas sweeps; the last one forms u^{n+1}
+        if (d == 3) {
+            PHASE(IB_PH_SWEEP_Y, launch_sweep_mid(s, 1));
+            PHASE(IB_PH_SWEEP_Z, launch_sweep_last(s, 2));
+        } else {
+            PHASE(IB_PH_SWEEP_Y, launch_sweep_last(s, 1));
+        }
+        // Step 3e: RHS and the psi factors (last axis first); Step 3f fused
+        PHASE(IB_PH_DIVPSI, launch_div_psi_first(s, d - 1));
+        if (d == 3) PHASE(IB_PH_PSI_Y, launch_psi_mid(s, 1));
+        PHASE(IB_PH_PSI_X, launch_psi_last_x(s));
+        for (int q = 0; q < d; ++q) {
             std::swap(s->u[q], s->st[q]);
             std::swap(s->nadv[q], s->nprev[q]);
         }
@@ -409,6 +430,22 @@ int ib_step(ib_ctx* c, int64_t nsteps)
             }
         }
     }
+    return IB_OK;
+}
+
+int ib_set_debug(ib_ctx* c, int32_t flags)
+{
+    if (!c) return fail(IB_EINVAL, "null context");
+    Ctx* s = &c->s;
+    const int keep = (flags & 1) != 0;
+    if (keep && !s->f[0]) {
+        const size_t fb = (size_t)s->ncell * sizeof(double);
+        for (int q = 0; q < s->dim; ++q) {
+            CKC(cudaMalloc(&s->f[q], fb));
+            CKC(cudaMemsetAsync(s->f[q], 0, fb, s->stream));
+        }
+    }
+    s->debug_keep_f = keep;
     return IB_OK;
 }
 
@@ -452,7 +489,11 @@ int ib_get_fields(ib_ctx* c, double* u, double* v, double* w, double* p, double*
     for (int q = 0; q < s->dim; ++q)
         if (out[q]) CKC(cudaMemcpyAsync(out[q], s->u[q], fb, cudaMemcpyDeviceToHost, s->stream));
     if (p) CKC(cudaMemcpyAsync(p, s->p, fb, cudaMemcpyDeviceToHost, s->stream));
-    if (psi) CKC(cudaMemcpyAsync(psi, s->psi, fb, cudaMemcpyDeviceToHost, s->stream));
+    if (psi) {
+        // the state keeps p* = p + psi; psi^{n-1/2} = p* - p
+        CKC(launch_sub(s, s->pstar, s->p, s->tmp));
+        CKC(cudaMemcpyAsync(psi, s->tmp, fb, cudaMemcpyDeviceToHost, s->stream));
+    }
     const size_t pb = (size_t)s->npts * s->dim * sizeof(double);
     if (X && pb) CKC(cudaMemcpyAsync(X, s->X, pb, cudaMemcpyDeviceToHost, s->stream));
     if (U && pb) CKC(cudaMemcpyAsync(U, s->Uprev, pb, cudaMemcpyDeviceToHost, s->stream));
@@ -468,6 +509,7 @@ int ib_get_aux(ib_ctx* c, double* fu, double* fv, double* fw, double* nu, double
     const size_t fb = (size_t)s->ncell * sizeof(double);
     double* fo[3] = {fu, fv, fw};
     double* no[3] = {nu, nv, nw};
+    if ((fu || fv || fw) && !s->debug_keep_f) return fail(IB_ESTATE, "f is only kept with ib_set_debug(ctx, 1)");
     for (int q = 0; q < s->dim; ++q) {
         if (fo[q]) CKC(cudaMemcpyAsync(fo[q], s->f[q], fb, cudaMemcpyDeviceToHost, s->stream));
         if (no[q]) CKC(cudaMemcpyAsync(no[q], s->nprev[q], fb, cudaMemcpyDeviceToHost, s->stream));
@@ -485,17 +527,14 @@ int ib_line_solve(ib_ctx* c, int32_t axis, double kappa, const double* d, double
     Ctx* s = &c->s;
     if (axis < 0 || axis >= s->dim) return fail(IB_EINVAL, "axis %d out of range", axis);
     if (!(kappa >= 0)) return fail(IB_EINVAL, "kappa must be >= 0");
-    make_line_coef(&s->hcoef[SYS_USER], s->n, s->L, -kappa, 1.0 + 2.0 * kappa, -kappa, 1);
+    static SchurInv hs;
+    make_line_coef(&s->hcoef[SYS_USER], &hs, s->n, s->L, -kappa, 1.0 + 2.0 * kappa, -kappa, 1);
     const size_t fb = (size_t)s->ncell * sizeof(double);
-    double* buf = nullptr;
-    CKC(cudaMalloc(&buf, fb));
-    CKC(cudaMemcpyAsync(s->coef + SYS_USER, &s->hcoef[SYS_USER], sizeof(LineCoef), cudaMemcpyHostToDevice, s->stream));
-    CKC(cudaMemcpyAsync(buf, d, fb, cudaMemcpyHostToDevice, s->stream));
-    cudaError_t e = launch_line_solve(s, axis, SYS_USER, buf);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(x, buf, fb, cudaMemcpyDeviceToHost, s->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
-    cudaFree(buf);
-    if (e != cudaSuccess) return fail(IB_ECUDA, "ib_line_solve: %s", cudaGetErrorString(e));
+    CKC(cudaMemcpyAsync(s->sinv + SYS_USER, &hs, sizeof(SchurInv), cudaMemcpyHostToDevice, s->stream));
+    CKC(cudaMemcpyAsync(s->tmp, d, fb, cudaMemcpyHostToDevice, s->stream));
+    CKC(launch_line_solve(s, axis, SYS_USER, s->tmp));
+    CKC(cudaMemcpyAsync(x, s->tmp, fb, cudaMemcpyDeviceToHost, s->stream));
+    CKC(cudaStreamSynchronize(s->stream));
     return IB_OK;
 }
 
@@ -527,7 +566,7 @@ int ib_destroy(ib_ctx* c)
     for (int q = 0; q < 3; ++q) {
         cudaFree(s->u[q]); cudaFree(s->st[q]); cudaFree(s->nadv[q]); cudaFree(s->nprev[q]); cudaFree(s->f[q]);
     }
-    cudaFree(s->p); cudaFree(s->psi); cudaFree(s->coef); cudaFree(s->d_flag);
+    cudaFree(s->p); cudaFree(s->pstar); cudaFree(s->tmp); cudaFree(s->sinv); cudaFree(s->d_flag);
     free_lagrangian(s);
     if (s->ev_made)
         for (int ph = 0; ph < IB_NPHASES; ++ph) { cudaEventDestroy(s->ev[ph][0]); cudaEventDestroy(s->ev[ph][1]); }

@@ -127,14 +127,19 @@ __global__ void k_force(const double* __restrict__ Xh, const int32_t* __restrict
 }
 
 // Step 2b: f_c += F_k,c w_k h^{-d} prod_a phi(X_a/h - I_a - o_{c,a}) at X^{n+1/2}
-// (PAPER.md:616-621); fp64 atomics into the zeroed f.
-template <int DIM, int KER>
+// (PAPER.md:616-621).  The force is accumulated (fp64 atomics) directly into the AB2
+// history G = N(u^{n-1}) + (2/rho) f that the momentum pass reads (R24), so
+// f is never cleared or re-read as a separate field; with keep_f it is also written
+// to f for ib_get_aux.
+template <int DIM, int KER, bool KEEP>
 __global__ void k_spread(const double* __restrict__ Xh, const double* __restrict__ F,
-                         const double* __restrict__ wgt, double* __restrict__ f0, double* __restrict__ f1,
-                         double* __restrict__ f2, int64_t npts, int n, double invh, double invhd)
+                         const double* __restrict__ wgt, double* __restrict__ g0, double* __restrict__ g1,
+                         double* __restrict__ g2, double* __restrict__ f0, double* __restrict__ f1,
+                         double* __restrict__ f2, int64_t npts, int n, double invh, double invhd, double two_rho)
 {
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k >= npts) return;
+    double* gc[3] = {g0, g1, g2};
     double* fc[3] = {f0, f1, f2};
     double Xk[3];
 #pragma unroll
@@ -154,7 +159,12 @@ __global__ void k_spread(const double* __restrict__ Xh, const double* __restrict
                 const size_t row = nn * (size_t)wrap1(i0[1] + m1, n);
                 const double a1 = Fc * w[1][m1];
 #pragma unroll
-                for (int m0 = 0; m0 < 4; ++m0) atomicAdd(fc[c] + row + wrap1(i0[0] + m0, n), a1 * w[0][m0]);
+                for (int m0 = 0; m0 < 4; ++m0) {
+                    const size_t q = row + wrap1(i0[0] + m0, n);
+                    const double v = a1 * w[0][m0];
+                    atomicAdd(gc[c] + q, two_rho * v);
+                    if (KEEP) atomicAdd(fc[c] + q, v);
+                }
             }
         } else {
 #pragma unroll
@@ -166,7 +176,12 @@ __global__ void k_spread(const double* __restrict__ Xh, const double* __restrict
                     const size_t row = pl + nn * (size_t)wrap1(i0[1] + m1, n);
                     const double a1 = a2 * w[1][m1];
 #pragma unroll
-                    for (int m0 = 0; m0 < 4; ++m0) atomicAdd(fc[c] + row + wrap1(i0[0] + m0, n), a1 * w[0][m0]);
+                    for (int m0 = 0; m0 < 4; ++m0) {
+                        const size_t q = row + wrap1(i0[0] + m0, n);
+                        const double v = a1 * w[0][m0];
+                        atomicAdd(gc[c] + q, two_rho * v);
+                        if (KEEP) atomicAdd(fc[c] + q, v);
+                    }
                 }
             }
         }
@@ -215,10 +230,18 @@ cudaError_t launch_spread(Ctx* s)
     const int thr = 128;
     const double invh = 1.0 / s->h;
     const double invhd = (s->dim == 3) ? invh * invh * invh : invh * invh;
-#define IBGM_SP(D, K) k_spread<D, K><<<nblk(s->npts, thr), thr, 0, s->stream>>>( \
-        s->Xh, s->F, s->wgt, s->f[0], s->f[1], s->f[2], s->npts, (int)s->n, invh, invhd)
-    if (s->dim == 2) { if (s->kernel == IB_DELTA_COS4) IBGM_SP(2, 0); else IBGM_SP(2, 1); }
-    else { if (s->kernel == IB_DELTA_COS4) IBGM_SP(3, 0); else IBGM_SP(3, 1); }
+    const double two_rho = 2.0 / s->rho;
+#define IBGM_SP(D, K, KP) k_spread<D, K, KP><<<nblk(s->npts, thr), thr, 0, s->stream>>>( \
+        s->Xh, s->F, s->wgt, s->nprev[0], s->nprev[1], s->nprev[2], s->f[0], s->f[1], s->f[2], s->npts, \
+        (int)s->n, invh, invhd, two_rho)
+    const bool kp = s->debug_keep_f != 0;
+    if (s->dim == 2) {
+        if (s->kernel == IB_DELTA_COS4) { if (kp) IBGM_SP(2, 0, true); else IBGM_SP(2, 0, false); }
+        else { if (kp) IBGM_SP(2, 1, true); else IBGM_SP(2, 1, false); }
+    } else {
+        if (s->kernel == IB_DELTA_COS4) { if (kp) IBGM_SP(3, 0, true); else IBGM_SP(3, 0, false); }
+        else { if (kp) IBGM_SP(3, 1, true); else IBGM_SP(3, 1, false); }
+    }
 #undef IBGM_SP
     s->launches++;
     return cudaGetLastError();

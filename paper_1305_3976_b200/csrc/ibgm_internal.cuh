@@ -16,18 +16,24 @@ constexpr int kMaxL = 32;     // max segment length L
 // solved by the paper's Schur-complement splitting applied
 // inside a thread block: each line of N = P*L unknowns is cut into P parts; part p
 // is one interface unknown y_p = x_{pL} followed by an interior block of m = L-1
-// unknowns (the B_p of eq. BlockSchurSystem).  Everything below is line-independent
+// unknowns (the B_p of eq. BlockSchurSystem).  Everything here is line-independent
 // and precomputed once on the host in long double (PAPER.md:1260-1262:
-// "S and B^{-1}E can be precomputed").
+// "S and B^{-1}E can be precomputed").  Passed to kernels BY VALUE (constant bank).
 struct LineCoef {
-    double c, a, b;           // sub, diag, super
+    double c, a, b;
     double inv_rowsum;        // 1/(a+b+c): mean(x) = mean(d)/(a+b+c) for circulant A
+    double gsum, hsum;        // sum_i g_i, sum_i h_i
     int L, P, N, mean_fix;
     double inv[kMaxL];        // Thomas: 1/den_i of B (i = 0..m-1)
     double cp[kMaxL];         // Thomas: b/den_i
     double g[kMaxL];          // B^{-1} e_1   (first column of B^{-1})
     double h[kMaxL];          // B^{-1} e_m   (last column of B^{-1})
-    double sinv[kMaxSeg * kMaxSeg];  // dense inverse of the P x P periodic Schur matrix S
+};
+
+// dense inverse of the P x P periodic Schur matrix S and its column sums (device)
+struct SchurInv {
+    double sinv[kMaxSeg * kMaxSeg];
+    double colsum[kMaxSeg];
 };
 
 enum SysId { SYS_VISC = 0, SYS_PSI = 1, SYS_USER = 2, SYS_COUNT = 3 };
@@ -39,17 +45,18 @@ struct Ctx {
     int kernel, advection, device;
     cudaStream_t stream;
     bool own_stream;
-    int L, P, R;                      // line segmentation: N = P*L, R lines per block
+    int L, P;                         // line segmentation: N = P*L
     // Eulerian state (device), each ncell doubles
     double* u[3];                     // u^n
-    double* st[3];                    // stage buffer: u**, u***, u^{n+1}
+    double* st[3];                    // Douglas increments delta1, delta2, then u^{n+1}
     double* nadv[3];                  // N(u^n), written this step
-    double* nprev[3];                 // N(u^{n-1})
-    double* f[3];                     // spread force f^{n+1/2}
+    double* nprev[3];                 // G = N(u^{n-1}) + (2/rho) f^{n+1/2} (spread adds f here)
+    double* f[3];                     // debug only: f^{n+1/2} kept for ib_get_aux
     double* p;                        // p^{n-1/2}  (holds q = p - chi mu D.u_bar mid-step)
-    double* psi;                      // psi^{n-1/2} (holds the psi RHS / factors mid-step)
-    LineCoef* coef;                   // device copies, SYS_COUNT entries
-    LineCoef hcoef[SYS_COUNT];        // host copies
+    double* pstar;                    // p* = p^{n-1/2} + psi^{n-1/2}; psi factors mid-step
+    double* tmp;                      // scratch field (ib_get_fields psi, ib_line_solve)
+    SchurInv* sinv;                   // device, SYS_COUNT entries
+    LineCoef hcoef[SYS_COUNT];        // host copies (passed by value)
     // Lagrangian state (device)
     int64_t npts, nedges;
     double *X, *Xh, *Uprev, *F, *wgt;   // Uprev: U interpolated in the last step
@@ -58,6 +65,7 @@ struct Ctx {
     double* csr_kappa;                // [2*nedges]
     double* csr_rest;                 // [2*nedges]
     int has_rest;
+    int debug_keep_f;                 // ib_set_debug: also accumulate f for ib_get_aux
     int64_t step;                     // steps completed since set_fields/set_boundary
     bool fields_set;
     int64_t launches;
@@ -72,18 +80,21 @@ struct Ctx {
 };
 
 // host-side precompute (api.cu)
-void make_line_coef(LineCoef* C, int64_t N, int L, double c, double a, double b, int mean_fix);
+void make_line_coef(LineCoef* C, SchurInv* S, int64_t N, int L, double c, double a, double b, int mean_fix);
 
 // launchers (fluid.cu)
-cudaError_t launch_s1_x(Ctx* s, int first_step);             // RHS + AB2 + x-sweep (Steps 3a-3c)
-cudaError_t launch_visc_sweep(Ctx* s, int axis);             // y or z Douglas sweep (Step 3d)
-cudaError_t launch_div(Ctx* s);                              // r = -(rho/dt) D.u^{n+1}; q = p - chi mu D.u_bar
-cudaError_t launch_psi_sweep(Ctx* s, int axis, int last);    // psi factor along axis; last: p = q + psi
+cudaError_t launch_s1_x(Ctx* s, int first_step);             // Steps 3a-3c: p*, momentum, x sweep
+cudaError_t launch_sweep_mid(Ctx* s, int axis);              // Step 3d: a middle Douglas sweep
+cudaError_t launch_sweep_last(Ctx* s, int axis);             // last Douglas sweep, u^{n+1} = u^n + delta
+cudaError_t launch_div_psi_first(Ctx* s, int axis);          // Step 3e RHS + first psi factor + q (3f)
+cudaError_t launch_psi_mid(Ctx* s, int axis);                // middle psi factor (3D)
+cudaError_t launch_psi_last_x(Ctx* s);                       // last psi factor, p = q + psi, p* = p + psi
 cudaError_t launch_line_solve(Ctx* s, int axis, int sys, double* data);  // stand-alone solve
+cudaError_t launch_sub(Ctx* s, const double* a, const double* b, double* out);  // out = a - b
 // IB (ib.cu)
 cudaError_t launch_interp_evolve(Ctx* s, int first_step);    // Steps 1a-1c
 cudaError_t launch_force(Ctx* s);                            // Step 2a
-cudaError_t launch_spread(Ctx* s);                           // Step 2b
+cudaError_t launch_spread(Ctx* s);                           // Step 2b (into G, and f in debug mode)
 cudaError_t launch_check_finite(Ctx* s);
 
 }  // namespace ibgm

@@ -39,10 +39,11 @@ class ib_options(ctypes.Structure):
 _lib = None
 SYMBOLS = ["ib_default_options", "ib_create", "ib_set_fields", "ib_set_boundary", "ib_set_fibers",
            "ib_step", "ib_sync", "ib_get_fields", "ib_get_aux", "ib_line_solve", "ib_check_finite",
-           "ib_get_stats", "ib_destroy", "ib_last_error", "ib_set_profiling", "ib_get_phase_times"]
+           "ib_get_stats", "ib_destroy", "ib_last_error", "ib_set_profiling", "ib_get_phase_times",
+           "ib_set_debug"]
 
-PHASES = ["interp_evolve", "force", "zero_f", "spread", "s1_rhs_xsweep", "visc_y", "visc_z", "div",
-          "psi_z", "psi_y", "psi_x_p"]
+PHASES = ["interp_evolve", "force", "spread", "s1_rhs_xsweep", "sweep_y", "sweep_z", "div_psi_first",
+          "psi_y", "psi_x_p", "clear"]
 
 
 def lib_path() -> str:
@@ -78,6 +79,7 @@ def lib():
         L.ib_last_error.restype = ctypes.c_char_p
         L.ib_set_profiling.argtypes = [ctypes.c_void_p, ctypes.c_int32]
         L.ib_get_phase_times.argtypes = [ctypes.c_void_p, _dp, _i64p]
+        L.ib_set_debug.argtypes = [ctypes.c_void_p, ctypes.c_int32]
         for name in SYMBOLS:
             if name not in ("ib_default_options", "ib_last_error"):
                 getattr(L, name).restype = ctypes.c_int
@@ -178,9 +180,9 @@ class Context:
         """D2H into caller buffers (e.g. pinned); any may be None."""
         _ck(lib().ib_get_fields(self._h, _p(u), _p(v), _p(w), _p(p), None, _p(X), None))
 
-    def aux(self):
+    def aux(self, with_f=True):
         d3 = self.dim == 3
-        f = [np.empty(self.shape) for _ in range(self.dim)]
+        f = [np.empty(self.shape) for _ in range(self.dim)] if with_f else [None] * 3
         nadv = [np.empty(self.shape) for _ in range(self.dim)]
         F = np.empty((self.npts, self.dim))
         Xh = np.empty((self.npts, self.dim))
@@ -197,6 +199,9 @@ class Context:
 
     def check_finite(self):
         _ck(lib().ib_check_finite(self._h))
+
+    def set_debug(self, keep_f: bool):
+        _ck(lib().ib_set_debug(self._h, int(keep_f)))
 
     def set_profiling(self, on: bool):
         _ck(lib().ib_set_profiling(self._h, int(on)))

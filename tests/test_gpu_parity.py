@@ -88,6 +88,7 @@ def test_one_step_stage_parity(cfg, over):
     pr = inputs.config(cfg, **over)
     o = _oracle_for(pr)
     g = _gpu_for(pr)
+    g.set_debug(True)          # keep f^{n+1/2} as a separate field for this comparison
     o.step(1)
     g.step(1)
     ao, ag = o.aux(), g.aux()
