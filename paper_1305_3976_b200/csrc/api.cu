@@ -238,11 +238,12 @@ int ib_create(const ib_grid* grid, double nu, double rho, double dt, const ib_op
     SchurInv hs[SYS_COUNT];
     // viscous Douglas sweeps: (1 - kap delta) with kap = mu dt / (2 rho h^2)
     const double kv = s->mu * dt / (2.0 * rho * s->h * s->h);
-    make_line_coef(&s->hcoef[SYS_VISC], &hs[SYS_VISC], s->n, L, -kv, 1.0 + 2.0 * kv, -kv, 1);
+    // (well conditioned, cond <= 1 + 4 kv: no mean correction needed, R16)
+    make_line_coef(&s->hcoef[SYS_VISC], &hs[SYS_VISC], s->n, L, -kv, 1.0 + 2.0 * kv, -kv, 0);
     // psi factors: (1 - D_aa) with D_aa = delta / h^2 (R2)
     const double kp = 1.0 / (s->h * s->h);
     make_line_coef(&s->hcoef[SYS_PSI], &hs[SYS_PSI], s->n, L, -kp, 1.0 + 2.0 * kp, -kp, 1);
-    make_line_coef(&s->hcoef[SYS_USER], &hs[SYS_USER], s->n, L, -kv, 1.0 + 2.0 * kv, -kv, 1);
+    make_line_coef(&s->hcoef[SYS_USER], &hs[SYS_USER], s->n, L, -kv, 1.0 + 2.0 * kv, -kv, 0);
     CKC(cudaMemcpyAsync(s->sinv, hs, sizeof(SchurInv) * SYS_COUNT, cudaMemcpyHostToDevice, s->stream));
     CKC(cudaStreamSynchronize(s->stream));
     return IB_OK;
@@ -528,7 +529,8 @@ int ib_line_solve(ib_ctx* c, int32_t axis, double kappa, const double* d, double
     if (axis < 0 || axis >= s->dim) return fail(IB_EINVAL, "axis %d out of range", axis);
     if (!(kappa >= 0)) return fail(IB_EINVAL, "kappa must be >= 0");
     static SchurInv hs;
-    make_line_coef(&s->hcoef[SYS_USER], &hs, s->n, s->L, -kappa, 1.0 + 2.0 * kappa, -kappa, 1);
+    // the exact mean correction is applied to the ill-conditioned systems (kappa > 1, R16)
+    make_line_coef(&s->hcoef[SYS_USER], &hs, s->n, s->L, -kappa, 1.0 + 2.0 * kappa, -kappa, kappa > 1.0 ? 1 : 0);
     const size_t fb = (size_t)s->ncell * sizeof(double);
     CKC(cudaMemcpyAsync(s->sinv + SYS_USER, &hs, sizeof(SchurInv), cudaMemcpyHostToDevice, s->stream));
     CKC(cudaMemcpyAsync(s->tmp, d, fb, cudaMemcpyHostToDevice, s->stream));

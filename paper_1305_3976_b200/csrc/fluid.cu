@@ -19,12 +19,14 @@
 //
 // Every line pass solves independent cyclic tridiagonal systems (eq. TriDiagX,
 // PAPER.md:985-995) with the paper's Schur-complement splitting
-// mapped onto one CTA: a line is cut into P parts of L unknowns; one thread per part
-// runs Thomas's algorithm on its interior block in registers, the P x P periodic
-// Schur system is solved with the precomputed dense S^{-1} through shared memory, and
-// each thread corrects x = f* - B^{-1} E y.  Strided (y, z) lines put neighbouring
-// lines on neighbouring lanes so every global access is coalesced; contiguous x lines
-// are staged through a padded shared-memory tile with coalesced loads and stores.
+// mapped onto one WARP: a line is cut into P parts of L unknowns and the P parts sit
+// in P lanes.  Each lane runs Thomas's algorithm on its interior block in registers
+// (the paper's "local tridiagonal solver"), the gather/scatter of the interface
+// values become register shuffles, the P x P periodic Schur
+// system is applied through the precomputed dense S^{-1}, and each lane corrects
+// x = f* - B^{-1} E y -- no block barrier inside the solve.  Every pass stages its
+// R lines x N positions through a segment-padded shared-memory tile, filled and
+// drained with coalesced global accesses (consecutive x for every axis).
 #include <cuda_runtime.h>
 
 #include <cstdio>
@@ -40,92 +42,101 @@ __device__ __forceinline__ double ldg(const double* p) { return __ldg(p); }
 template <typename T>
 __device__ __forceinline__ T pick3(T a, T b, T c, int i) { return i == 0 ? a : (i == 1 ? b : c); }
 
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// cp.async (LDGSTS) of one double global -> shared, cached in L1/L2; completes at
+// cp_async_wait_all().  Lets a thread keep all its tile loads in flight at once.
+__device__ __forceinline__ void cp_async8(double* sdst, const double* gsrc)
+{
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all()
+{
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
 // -------------------------------------------------------------------------------
-// Schur-segmented solve of NC independent lines' parts (one part per thread and
-// component).  On entry x[k][0..L-1] holds the right-hand side of rows sL..sL+L-1;
-// on exit the solution.  Block-uniform control flow (2 __syncthreads).
-//   sh layout: per component k: first[PR] last[PR] r[PR] e[PR]   (PR = P*R)
+// Staged tile: R lines x N positions; segment s of a line (L positions) occupies L+1
+// doubles so that lanes holding consecutive segments of a line hit distinct banks,
+// and the line pitch TP is odd so that consecutive lines do too.
 // -------------------------------------------------------------------------------
-template <int L, int NC>
-__device__ __forceinline__ void schur_solve(double (&x)[NC][L], const LineCoef& C, int s, int l, int R, int P,
-                                            const double* __restrict__ sh_sinv, const double* __restrict__ sh_cs,
-                                            double* sh)
+__host__ __device__ inline int tile_pitch(int P, int L)
+{
+    const int tp = P * (L + 1);
+    return (tp % 2 == 0) ? tp + 1 : tp;
+}
+
+template <int L>
+__device__ __forceinline__ int tile_off(int l, int m, int TP)
+{
+    const int s = m / L;
+    return l * TP + s * (L + 1) + (m - s * L);
+}
+
+template <int P2>
+__device__ __forceinline__ double group_sum(double v, int P, int gbase)
+{
+    if ((P & (P - 1)) == 0) {
+        for (int off = P >> 1; off >= 1; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
+        return v;
+    }
+    double t = 0.0;
+    for (int q = 0; q < P; ++q) t += __shfl_sync(kFull, v, gbase + q);
+    return t;
+}
+
+// -------------------------------------------------------------------------------
+// Warp-synchronous Schur-segmented solve of one part (L unknowns, rows sL..sL+L-1)
+// of a cyclic line whose P parts sit in lanes gbase .. gbase+P-1.  All 32 lanes of
+// the warp must call it.
+// -------------------------------------------------------------------------------
+template <int L>
+__device__ __forceinline__ void ws_solve(double (&x)[L], const LineCoef& C, int s, int P, int gbase,
+                                         const double* __restrict__ sinvT)
 {
     constexpr int M = L - 1;
     const double c = C.c, b = C.b;
-    const int PR = P * R;
-    const int me = s * R + l;
-    const int sm1 = (s == 0) ? P - 1 : s - 1;
-    const int sp1 = (s == P - 1) ? 0 : s + 1;
     const bool mf = C.mean_fix != 0;
+    double dsum = 0.0;
+    if (mf) {
 #pragma unroll
-    for (int k = 0; k < NC; ++k) {
-        double dsum = 0.0;
-        if (mf) {
-#pragma unroll
-            for (int i = 0; i < L; ++i) dsum += x[k][i];
-        }
-        // f*_p = B_p^{-1} f_p  (eq. LocalTriSystem; Thomas)
-        x[k][1] *= C.inv[0];
-#pragma unroll
-        for (int i = 2; i <= M; ++i) x[k][i] = (x[k][i] - c * x[k][i - 1]) * C.inv[i - 1];
-#pragma unroll
-        for (int i = M - 1; i >= 1; --i) x[k][i] -= C.cp[i - 1] * x[k][i + 1];
-        double* shk = sh + 4 * PR * k;
-        // gather first/last entries of f*_p
-        shk[me] = x[k][1];
-        shk[PR + me] = x[k][M];
-        if (mf) {
-            double fsum = 0.0;
-#pragma unroll
-            for (int i = 1; i <= M; ++i) fsum += x[k][i];
-            shk[3 * PR + me] = dsum * C.inv_rowsum - fsum;
-        }
+        for (int i = 0; i < L; ++i) dsum += x[i];
     }
-    __syncthreads();
+    // f*_p = B_p^{-1} f_p  (eq. LocalTriSystem; Thomas)
+    x[1] *= C.inv[0];
 #pragma unroll
-    for (int k = 0; k < NC; ++k) {
-        double* shk = sh + 4 * PR * k;
-        // right-hand side of the Schur system  g - F f*  (eq. SchurSystem)
-        shk[2 * PR + me] = x[k][0] - c * shk[PR + sm1 * R + l] - b * shk[me];
+    for (int i = 2; i <= M; ++i) x[i] = (x[i] - c * x[i - 1]) * C.inv[i - 1];
+#pragma unroll
+    for (int i = M - 1; i >= 1; --i) x[i] -= C.cp[i - 1] * x[i + 1];
+    // gather: the interface row p couples to the last entry of f*_{p-1} and the first
+    // of f*_p; r = g - F f*  (eq. SchurSystem)
+    const int sprev = gbase + ((s == 0) ? P - 1 : s - 1);
+    const int snext = gbase + ((s == P - 1) ? 0 : s + 1);
+    const double fl_prev = __shfl_sync(kFull, x[M], sprev);
+    const double r = x[0] - c * fl_prev - b * x[1];
+    // y = S^{-1} r  (S precomputed); this part needs y_p, y_{p+1}
+    double ys = 0.0;
+    for (int q = 0; q < P; ++q) ys = fma(sinvT[q * P + s], __shfl_sync(kFull, r, gbase + q), ys);
+    const double ys1 = __shfl_sync(kFull, ys, snext);
+    // correction x_p = f*_p - B_p^{-1} E_p y, E_p y = c y_p e_1 + b y_{p+1} e_m
+    x[0] = ys;
+    const double cy = c * ys, by = b * ys1;
+#pragma unroll
+    for (int i = 1; i <= M; ++i) x[i] -= cy * C.g[i - 1] + by * C.h[i - 1];
+    if (mf) {
+        // exact line-mean correction (R16): 1^T A = (a+b+c) 1^T, so
+        // sum(x) must equal sum(d)/(a+b+c)
+        double xs = 0.0;
+#pragma unroll
+        for (int i = 0; i < L; ++i) xs += x[i];
+        const double D = group_sum<0>(dsum, P, gbase);
+        const double X = group_sum<0>(xs, P, gbase);
+        const double corr = (D * C.inv_rowsum - X) / (double)(P * L);
+#pragma unroll
+        for (int i = 0; i < L; ++i) x[i] += corr;
     }
-    __syncthreads();
-    const double* Si = sh_sinv + s * P;
-    const double* Si1 = sh_sinv + sp1 * P;
-#pragma unroll
-    for (int k = 0; k < NC; ++k) {
-        const double* shk = sh + 4 * PR * k;
-        // y = S^{-1}(g - F f*); this part needs y_p and y_{p+1}
-        double ys = 0.0, ys1 = 0.0, ysum = 0.0, E = 0.0;
-        for (int q = 0; q < P; ++q) {
-            const double r = shk[2 * PR + q * R + l];
-            ys = fma(Si[q], r, ys);
-            ys1 = fma(Si1[q], r, ys1);
-            if (mf) {
-                ysum = fma(sh_cs[q], r, ysum);
-                E += shk[3 * PR + q * R + l];
-            }
-        }
-        // x_p = f*_p - B_p^{-1} E_p y; E_p y = c y_p e_1 + b y_{p+1} e_m
-        x[k][0] = ys;
-        const double cy = c * ys, by = b * ys1;
-#pragma unroll
-        for (int i = 1; i <= M; ++i) x[k][i] -= cy * C.g[i - 1] + by * C.h[i - 1];
-        if (mf) {
-            // exact line-mean correction (R16): 1^T A = (a+b+c) 1^T, so
-            // sum(x) must equal sum(d)/(a+b+c).  sum over the line of the computed x is
-            // (1 - c sum g - b sum h) sum_p y_p + sum_p sum f*_p  (no third barrier).
-            const double corr = (E - (1.0 - c * C.gsum - b * C.hsum) * ysum) / (double)(P * L);
-#pragma unroll
-            for (int i = 0; i < L; ++i) x[k][i] += corr;
-        }
-    }
-}
-
-__device__ __forceinline__ void load_sinv(const SchurInv* __restrict__ SI, int P, double* sh_sinv, double* sh_cs)
-{
-    for (int e = threadIdx.x; e < P * P; e += blockDim.x) sh_sinv[e] = SI->sinv[e];
-    for (int e = threadIdx.x; e < P; e += blockDim.x) sh_cs[e] = SI->colsum[e];
 }
 
 // -------------------------------------------------------------------------------
@@ -141,36 +152,60 @@ struct S1Args {
     int first, advection;
 };
 
+// Row bases of one x-row (j, k) and its y/z neighbours, 32-bit flat offsets.
+struct RowB {
+    unsigned r0, ryp, rym, rzp, rzm, rypzm, rymzp;
+};
+
 template <int DIM>
-__device__ __forceinline__ void s1_cell(const S1Args& A, int i, int j, int k, int n, double (&d)[3])
+__device__ __forceinline__ RowB row_bases(int j, int k, int n)
 {
-    const size_t N = (size_t)n;
-    const int im = (i == 0) ? n - 1 : i - 1, ip = (i == n - 1) ? 0 : i + 1;
-    const size_t rj = N * j, rjm = N * (size_t)((j == 0) ? n - 1 : j - 1), rjp = N * (size_t)((j == n - 1) ? 0 : j + 1);
-    size_t rk = 0, rkm = 0, rkp = 0;
+    const unsigned N = (unsigned)n, NN = N * N;
+    const unsigned jm = (j == 0) ? n - 1 : j - 1, jp = (j == n - 1) ? 0 : j + 1;
+    RowB b;
+    unsigned kk = 0, km = 0, kp = 0;
     if (DIM == 3) {
-        rk = N * N * k;
-        rkm = N * N * (size_t)((k == 0) ? n - 1 : k - 1);
-        rkp = N * N * (size_t)((k == n - 1) ? 0 : k + 1);
+        kk = NN * (unsigned)k;
+        km = NN * (unsigned)((k == 0) ? n - 1 : k - 1);
+        kp = NN * (unsigned)((k == n - 1) ? 0 : k + 1);
     }
+    b.r0 = N * j + kk;
+    b.ryp = N * jp + kk;
+    b.rym = N * jm + kk;
+    b.rzp = N * j + kp;
+    b.rzm = N * j + km;
+    b.rypzm = N * jp + km;
+    b.rymzp = N * jm + kp;
+    return b;
+}
+
+// Skew-symmetric advection (Morinishi "Skew.-S2", R4).  With
+// T = u_j averaged in c, A = u_c averaged in j and g = d_j u_c at the faces I -/+ h/2 e_j,
+// (1/2)[ sum_j (TA|+ - TA|-)/h + sum_j (Tg|- + Tg|+)/2 ] collapses exactly (the u_c(I)
+// terms cancel) to
+//   N_c = 1/(4h) sum_j [ (u_j(I+e_j) + u_j(I+e_j-e_c)) u_c(I+e_j) - (u_j(I) + u_j(I-e_c)) u_c(I-e_j) ]
+template <int DIM>
+__device__ __forceinline__ void s1_cell(const S1Args& A, int i, const RowB& rb, int n, double (&d)[3])
+{
+    const unsigned im = (i == 0) ? n - 1 : i - 1, ip = (i == n - 1) ? 0 : i + 1, ii = (unsigned)i;
     // offsets of I, I+e_x, I-e_x, I+e_y, I-e_y, I+e_z, I-e_z  (index 0, 1+2a, 2+2a)
-    size_t o[7];
-    o[0] = i + rj + rk;
-    o[1] = ip + rj + rk;
-    o[2] = im + rj + rk;
-    o[3] = i + rjp + rk;
-    o[4] = i + rjm + rk;
-    o[5] = i + rj + rkp;
-    o[6] = i + rj + rkm;
+    unsigned o[7];
+    o[0] = ii + rb.r0;
+    o[1] = ip + rb.r0;
+    o[2] = im + rb.r0;
+    o[3] = ii + rb.ryp;
+    o[4] = ii + rb.rym;
+    o[5] = ii + rb.rzp;
+    o[6] = ii + rb.rzm;
     // I + e_m - e_c  (m != c)
-    size_t mx[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
-    mx[0][1] = ip + rjm + rk;
-    mx[1][0] = im + rjp + rk;
+    unsigned mx[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+    mx[0][1] = ip + rb.rym;
+    mx[1][0] = im + rb.ryp;
     if (DIM == 3) {
-        mx[0][2] = ip + rj + rkm;
-        mx[1][2] = i + rjp + rkm;
-        mx[2][0] = im + rj + rkp;
-        mx[2][1] = i + rjm + rkp;
+        mx[0][2] = ip + rb.rzm;
+        mx[1][2] = ii + rb.rypzm;
+        mx[2][0] = im + rb.rzp;
+        mx[2][1] = ii + rb.rymzp;
     }
     constexpr int NO = 1 + 2 * DIM;
     double U[DIM][NO];
@@ -180,7 +215,7 @@ __device__ __forceinline__ void s1_cell(const S1Args& A, int i, int j, int k, in
 #pragma unroll
         for (int q = 0; q < NO; ++q) U[m][q] = ldg(A.u[m] + o[q]);
 #pragma unroll
-        for (int c = 0; c < DIM; ++c) X[m][c] = (c == m) ? 0.0 : ldg(A.u[m] + mx[m][c]);
+        for (int c = 0; c < DIM; ++c) X[m][c] = (c == m || !A.advection) ? 0.0 : ldg(A.u[m] + mx[m][c]);
     }
     double ps0 = 0.0, psm[3] = {0, 0, 0};
     if (!A.first) {
@@ -189,224 +224,211 @@ __device__ __forceinline__ void s1_cell(const S1Args& A, int i, int j, int k, in
         for (int c = 0; c < DIM; ++c) psm[c] = ldg(A.pstar + o[2 + 2 * c]);
     }
     const double invh = A.invh;
+    const double dt_rho = A.dt * A.inv_rho;
 #pragma unroll
     for (int c = 0; c < DIM; ++c) {
         const double u0 = U[c][0];
-        // skew-symmetric advection, Morinishi "Skew.-S2" (R4)
         double Nc = 0.0;
         if (A.advection) {
-            double dv = 0.0, ad = 0.0;
 #pragma unroll
             for (int jd = 0; jd < DIM; ++jd) {
-                const double ucm = U[c][2 + 2 * jd], ucp = U[c][1 + 2 * jd];
-                const double Tm = 0.5 * (U[jd][0] + U[jd][2 + 2 * c]);
-                const double Tp = 0.5 * (U[jd][1 + 2 * jd] + ((jd == c) ? u0 : X[jd][c]));
-                const double Am = 0.5 * (u0 + ucm), Ap = 0.5 * (ucp + u0);
-                const double Gm = (u0 - ucm) * invh, Gp = (ucp - u0) * invh;
-                dv += (Tp * Ap - Tm * Am) * invh;
-                ad += 0.5 * (Tm * Gm + Tp * Gp);
+                const double Tp = U[jd][1 + 2 * jd] + ((jd == c) ? u0 : X[jd][c]);
+                const double Tm = U[jd][0] + U[jd][2 + 2 * c];
+                Nc = fma(Tp, U[c][1 + 2 * jd], Nc);
+                Nc = fma(-Tm, U[c][2 + 2 * jd], Nc);
             }
-            Nc = 0.5 * (dv + ad);
+            Nc *= 0.25 * invh;
         }
         A.nadv[c][o[0]] = Nc;
         double lap = 0.0;
 #pragma unroll
-        for (int a = 0; a < DIM; ++a) lap += U[c][1 + 2 * a] - 2.0 * u0 + U[c][2 + 2 * a];
-        lap *= invh * invh;
+        for (int a = 0; a < DIM; ++a) lap += U[c][1 + 2 * a] + U[c][2 + 2 * a];
+        lap = (lap - 2.0 * DIM * u0) * (invh * invh);
         const double gp = A.first ? 0.0 : (ps0 - psm[c]) * invh;     // G^{C->E} p*
         const double Gc = ldg(A.G[c] + o[0]);
         // u* - u^n = dt ( -3/2 N + 1/2 G + (mu lap - G p*)/rho ),  G carries f
-        d[c] = A.dt * (-A.a1 * Nc + 0.5 * Gc + (A.mu * lap - gp) * A.inv_rho);
+        d[c] = A.dt * (0.5 * Gc - A.a1 * Nc) + dt_rho * (A.mu * lap - gp);
     }
 }
 
 // -------------------------------------------------------------------------------
-// x-line kernels: R consecutive rows (j0..j0+R-1 at fixed k) staged in padded shared
-// tiles [NC][R][N+1]; thread t -> row l = t % R, part s = t / R.
+// The line-pass kernel.  AX: line axis (0 = x, rows of R consecutive j at fixed k;
+// 1 = y / 2 = z, R consecutive i at fixed k / j).  NC tiles are staged (NC = DIM for
+// S1, else 1 with the component in blockIdx.z).
 // -------------------------------------------------------------------------------
-enum XOp { XOP_S1 = 0, XOP_PSI_LAST = 1, XOP_USER = 2 };
+enum Kind { K_S1 = 0, K_MID = 1, K_LAST = 2, K_DIVPSI = 3, K_PSI_LAST = 4, K_USER = 5 };
 
-struct XArgs {
-    const double* in;
-    double* out;     // PSI_LAST: p* ; USER: x
-    double* p;       // PSI_LAST: holds q, becomes p^{n+1/2}
-};
-
-template <int L, int OP, int DIM, int NCB>
-__global__ void __launch_bounds__(512) k_line_x(const LineCoef C, const SchurInv* __restrict__ SI, int n, int R,
-                                                 S1Args s1, XArgs xa)
-{
-    constexpr int NC = (OP == XOP_S1) ? DIM : 1;   // components in the tile; NCB solved jointly
-    extern __shared__ double smem[];
-    const int P = C.P;
-    const int pitch = n + 1;
-    double* sh_sinv = smem;
-    double* sh_cs = sh_sinv + P * P;
-    double* tile = sh_cs + P;
-    double* red = tile + (size_t)NC * R * pitch;
-    const int t = threadIdx.x, nthr = blockDim.x;
-    const int l = t % R, s = t / R;
-    const int j0 = blockIdx.x * R;
-    const int k = blockIdx.y;
-    const size_t plane = (size_t)n * n;
-    load_sinv(SI, P, sh_sinv, sh_cs);
-
-    // fill (coalesced along x)
-    for (int e = t; e < R * n; e += nthr) {
-        const int row = e / n, i = e - row * n;
-        const int j = j0 + row;
-        double v[3] = {0.0, 0.0, 0.0};
-        if (j < n) {
-            if (OP == XOP_S1) {
-                s1_cell<DIM>(s1, i, j, k, n, v);
-            } else {
-                v[0] = ldg(xa.in + (size_t)i + (size_t)n * j + plane * k);
-            }
-        }
-#pragma unroll
-        for (int c = 0; c < NC; ++c) tile[(size_t)c * R * pitch + row * pitch + i] = v[c];
-    }
-    __syncthreads();
-#pragma unroll
-    for (int c0 = 0; c0 < NC; c0 += NCB) {
-        double x[NCB][L];
-#pragma unroll
-        for (int c = 0; c < NCB; ++c)
-#pragma unroll
-            for (int i = 0; i < L; ++i) x[c][i] = tile[(size_t)(c0 + c) * R * pitch + l * pitch + s * L + i];
-        schur_solve<L, NCB>(x, C, s, l, R, P, sh_sinv, sh_cs, red);
-#pragma unroll
-        for (int c = 0; c < NCB; ++c)
-#pragma unroll
-            for (int i = 0; i < L; ++i) tile[(size_t)(c0 + c) * R * pitch + l * pitch + s * L + i] = x[c][i];
-    }
-    __syncthreads();
-    // store (coalesced along x)
-    for (int e = t; e < R * n; e += nthr) {
-        const int row = e / n, i = e - row * n;
-        const int j = j0 + row;
-        if (j < n) {
-            const size_t q = (size_t)i + (size_t)n * j + plane * k;
-            if (OP == XOP_S1) {
-#pragma unroll
-                for (int c = 0; c < NC; ++c) s1.out[c][q] = tile[(size_t)c * R * pitch + row * pitch + i];
-            } else if (OP == XOP_PSI_LAST) {
-                const double psi = tile[row * pitch + i];
-                const double pn = xa.p[q] + psi;        // Step 3f: p^{n+1/2} = q + psi^{n+1/2}
-                xa.p[q] = pn;
-                xa.out[q] = pn + psi;                   // Step 3a of the next step: p* = p + psi
-            } else {
-                xa.out[q] = tile[row * pitch + i];
-            }
-        }
-    }
-}
-
-// -------------------------------------------------------------------------------
-// y/z-line kernel: R neighbouring lines (consecutive i) per block, direct coalesced
-// global access; thread t -> line l = t % R, part s = t / R.
-// -------------------------------------------------------------------------------
-enum YOp { YOP_MID = 0, YOP_LAST = 1, YOP_DIVPSI = 2 };
-
-struct YArgs {
-    double* io[3];          // MID: in/out increments; LAST: in increments, out u^{n+1}; DIVPSI: out psi
-    const double* un[3];    // LAST / DIVPSI: u^n
+struct LArgs {
+    S1Args s1;
+    double* io[3];          // MID/USER: in-place data; LAST: increments in, u^{n+1} out; DIVPSI: psi out
+    const double* un[3];    // LAST, DIVPSI: u^n
     const double* unew[3];  // DIVPSI: u^{n+1}
-    double* p;              // DIVPSI: p -> q
+    double* p;              // DIVPSI: p -> q ; PSI_LAST: q -> p^{n+1/2}
+    double* pstar;          // PSI_LAST: psi in, p* out
     double neg_rho_dt, chimu_half, invh;
 };
 
-template <int L, int NC, int OP, int DIM, int AX>
-__global__ void __launch_bounds__(512) k_line_yz(const LineCoef C, const SchurInv* __restrict__ SI, int n, int R,
-                                                  YArgs A)
+// Visit every (line l, position m) of the block's tile with coalesced global offsets:
+// consecutive threads take consecutive x.  f(l, m, q) with q the 32-bit flat index.
+template <int AX, class F>
+__device__ __forceinline__ void for_tile(int n, int R, int g0, unsigned tb, F&& f)
 {
-    // NC components per block, starting at component blockIdx.z * NC; AX = line axis (1 or 2)
-    constexpr int axis = AX;
-    const int c0 = blockIdx.z * NC;
-    extern __shared__ double smem[];
-    const int P = C.P;
-    double* sh_sinv = smem;
-    double* sh_cs = sh_sinv + P * P;
-    double* red = sh_cs + P;
-    const int t = threadIdx.x;
-    const int l = t % R, s = t / R;
-    const int i = blockIdx.x * R + l;
-    const bool active = i < n;
-    const int ii = active ? i : 0;
-    const size_t N = (size_t)n;
-    const size_t S = (AX == 1) ? N : N * N;          // stride along the line
-    const size_t T = (AX == 1) ? N * N : N;          // stride of the transverse index
-    const size_t base = (size_t)ii + T * blockIdx.y;
-    const int pos0 = s * L;
-    load_sinv(SI, P, sh_sinv, sh_cs);
-
-    double x[NC][L];
-    if (OP == YOP_DIVPSI) {
-        // D.u at the cells of this part for u^{n+1} and u^n; the
-        // line axis component's +1 neighbour is the next position along the line.
-        const size_t dxp = (ii == n - 1) ? (size_t)0 - (N - 1) : (size_t)1;               // +e_x offset
-        const size_t dyp = (blockIdx.y == (unsigned)(n - 1)) ? (size_t)0 - (N - 1) * N : N; // +e_y (3D z-lines)
-        double pn[L + 1];
-#pragma unroll
-        for (int m = 0; m <= L; ++m) pn[m] = 0.0;
-        double dn[L], dol[L];
-#pragma unroll
-        for (int m = 0; m < L; ++m) { dn[m] = 0.0; dol[m] = 0.0; }
-        // line-axis component: values at positions pos0 .. pos0+L (wrapped)
-        {
-            const double* a1 = A.unew[axis];
-            const double* a0 = A.un[axis];
-            double v1[L + 1], v0[L + 1];
-#pragma unroll
-            for (int m = 0; m <= L; ++m) {
-                const size_t q = base + S * (size_t)wrapn(pos0 + m, n);
-                v1[m] = ldg(a1 + q);
-                v0[m] = ldg(a0 + q);
+    const int t = threadIdx.x, T = blockDim.x;
+    const unsigned N = (unsigned)n;
+    if (AX == 0) {
+        if (n >= T) {
+            for (int l = 0; l < R; ++l) {
+                if (g0 + l >= n) break;
+                const unsigned rb = N * (unsigned)(g0 + l) + N * N * tb;
+                for (int m = t; m < n; m += T) f(l, m, rb + (unsigned)m);
             }
-#pragma unroll
-            for (int m = 0; m < L; ++m) { dn[m] += v1[m + 1] - v1[m]; dol[m] += v0[m + 1] - v0[m]; }
-        }
-#pragma unroll
-        for (int c = 0; c < DIM; ++c) {
-            if (c == axis) continue;
-            const size_t off = (c == 0) ? dxp : dyp;
-            const double* a1 = A.unew[c];
-            const double* a0 = A.un[c];
-#pragma unroll
-            for (int m = 0; m < L; ++m) {
-                const size_t q = base + S * (size_t)(pos0 + m);
-                dn[m] += ldg(a1 + q + off) - ldg(a1 + q);
-                dol[m] += ldg(a0 + q + off) - ldg(a0 + q);
-            }
-        }
-#pragma unroll
-        for (int m = 0; m < L; ++m) {
-            const size_t q = base + S * (size_t)(pos0 + m);
-            const double dnew = dn[m] * A.invh, dold = dol[m] * A.invh;
-            x[0][m] = A.neg_rho_dt * dnew;                             // Step 3e RHS
-            if (active) A.p[q] = A.p[q] - A.chimu_half * (dnew + dold);  // Step 3f, explicit part
+        } else {
+            const int rows = T / n;          // rows covered per sweep of the block
+            const int l0 = t / n, m = t - l0 * n;
+            if (l0 >= rows) return;
+            for (int l = l0; l < R && g0 + l < n; l += rows) f(l, m, (unsigned)m + N * (unsigned)(g0 + l) + N * N * tb);
         }
     } else {
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-            const double* in = pick3<double*>(A.io[0], A.io[1], A.io[2], c0 + c);
-#pragma unroll
-            for (int m = 0; m < L; ++m) x[c][m] = ldg(in + base + S * (size_t)(pos0 + m));
-        }
+        const int lg = 31 - __clz(R);        // R is a power of two
+        const int l = t & (R - 1);
+        if (g0 + l >= n) return;
+        const int mstep = T >> lg;
+        const unsigned S = (AX == 1) ? N : N * N;
+        const unsigned base = (unsigned)(g0 + l) + ((AX == 1) ? N * N * tb : N * tb);
+        for (int m = t >> lg; m < n; m += mstep) f(l, m, base + S * (unsigned)m);
     }
-    schur_solve<L, NC>(x, C, s, l, R, P, sh_sinv, sh_cs, red);
-    if (active) {
+}
+
+template <int L, int KIND, int DIM, int AX, int NC, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_lines(const LineCoef C, const SchurInv* __restrict__ SI, int n, int R,
+                                                     LArgs A)
+{
+    extern __shared__ double smem[];
+    const int P = C.P;
+    const int TP = tile_pitch(P, L);
+    double* sinvT = smem;
+    double* tile = smem + P * P;
+    double* tile2 = tile + (size_t)NC * R * TP;   // LAST: u^n, PSI_LAST: q (prefetched with the fill)
+    const int t = threadIdx.x, T = blockDim.x;
+    for (int e = t; e < P * P; e += T) {
+        const int q = e / P, sg = e - q * P;
+        sinvT[q * P + sg] = SI->sinv[sg * P + q];
+    }
+    const unsigned N = (unsigned)n;
+    const int comp = (NC == 1) ? blockIdx.z : 0;
+    const int g0 = blockIdx.x * R;              // first j (AX = 0) or first i (AX = 1, 2)
+    const unsigned tb = blockIdx.y;             // k (AX = 0, 1 in 3D) or j (AX = 2)
+    const unsigned RTP = (unsigned)R * TP;
+
+    // ---------------- fill (coalesced: consecutive threads -> consecutive x)
+    if (KIND == K_S1) {
+        if (n >= T) {
+            for (int l = 0; l < R && g0 + l < n; ++l) {
+                const RowB rb = row_bases<DIM>(g0 + l, (int)tb, n);
+                for (int m = t; m < n; m += T) {
+                    double v[3];
+                    s1_cell<DIM>(A.s1, m, rb, n, v);
+                    const int off = tile_off<L>(l, m, TP);
 #pragma unroll
-        for (int c = 0; c < NC; ++c) {
-            double* out = pick3<double*>(A.io[0], A.io[1], A.io[2], c0 + c);
-            const double* un = pick3<const double*>(A.un[0], A.un[1], A.un[2], c0 + c);
+                    for (int c = 0; c < NC; ++c) tile[c * RTP + off] = v[c];
+                }
+            }
+        } else {
+            const int rows = T / n;
+            const int l0 = t / n, m = t - l0 * n;
+            if (l0 < rows)
+                for (int l = l0; l < R && g0 + l < n; l += rows) {
+                    const RowB rb = row_bases<DIM>(g0 + l, (int)tb, n);
+                    double v[3];
+                    s1_cell<DIM>(A.s1, m, rb, n, v);
+                    const int off = tile_off<L>(l, m, TP);
 #pragma unroll
-            for (int m = 0; m < L; ++m) {
-                const size_t q = base + S * (size_t)(pos0 + m);
-                if (OP == YOP_LAST) out[q] = ldg(un + q) + x[c][m];   // u^{n+1} = u^n + d
-                else out[q] = x[c][m];
+                    for (int c = 0; c < NC; ++c) tile[c * RTP + off] = v[c];
+                }
+        }
+    } else if (KIND == K_DIVPSI) {
+        // D.u at each cell for u^{n+1} and u^n
+        const unsigned stp[3] = {1u, N, N * N};
+        for_tile<AX>(n, R, g0, tb, [&](int l, int m, unsigned q) {
+            // cell coordinates along each axis: i = g0 + l; the line axis coordinate is m
+            int ijk[3];
+            ijk[0] = g0 + l;
+            if (AX == 1) { ijk[1] = m; ijk[2] = (int)tb; } else { ijk[1] = (int)tb; ijk[2] = m; }
+            double dn = 0.0, dol = 0.0;
+#pragma unroll
+            for (int c = 0; c < DIM; ++c) {
+                const unsigned qp = (ijk[c] == n - 1) ? q - (N - 1) * stp[c] : q + stp[c];
+                dn += ldg(A.unew[c] + qp) - ldg(A.unew[c] + q);
+                dol += ldg(A.un[c] + qp) - ldg(A.un[c] + q);
+            }
+            dn *= A.invh;
+            dol *= A.invh;
+            tile[tile_off<L>(l, m, TP)] = A.neg_rho_dt * dn;         // Step 3e RHS
+            A.p[q] = A.p[q] - A.chimu_half * (dn + dol);             // Step 3f, explicit part
+        });
+    } else {
+        // pure copies: cp.async keeps every load of the tile in flight at once
+        const double* src = (KIND == K_PSI_LAST) ? A.pstar : pick3<double*>(A.io[0], A.io[1], A.io[2], comp);
+        const double* src2 = (KIND == K_LAST) ? pick3<const double*>(A.un[0], A.un[1], A.un[2], comp)
+                                              : (KIND == K_PSI_LAST ? A.p : nullptr);
+        for_tile<AX>(n, R, g0, tb, [&](int l, int m, unsigned q) {
+            const int off = tile_off<L>(l, m, TP);
+            cp_async8(tile + off, src + q);
+            if (KIND == K_LAST || KIND == K_PSI_LAST) cp_async8(tile2 + off, src2 + q);
+        });
+        cp_async_wait_all();
+    }
+    __syncthreads();
+
+    // ---------------- solve: warp-synchronous, P lanes per line
+    {
+        const int lane = t & 31, w = t >> 5, nw = T >> 5;
+        const int lpw = (P <= 32) ? 32 / P : 1;          // lines per warp per round
+        const int sub = lane / P;
+        const int s = lane - sub * P;
+        const int gbase = sub * P;
+        for (int lb = w * lpw; lb < R; lb += nw * lpw) {
+            const int l = lb + sub;
+            const bool ok = (sub < lpw) && (l < R);
+            const int lc = ok ? l : lb;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                double* tl = tile + c * RTP + lc * TP + s * (L + 1);
+                double x[L];
+#pragma unroll
+                for (int i = 0; i < L; ++i) x[i] = tl[i];
+                ws_solve<L>(x, C, s, P, gbase, sinvT);
+                if (ok) {
+#pragma unroll
+                    for (int i = 0; i < L; ++i) tl[i] = x[i];
+                }
             }
         }
+    }
+    __syncthreads();
+
+    // ---------------- store (coalesced)
+    if (KIND == K_S1) {
+        for_tile<AX>(n, R, g0, tb, [&](int l, int m, unsigned q) {
+            const int off = tile_off<L>(l, m, TP);
+#pragma unroll
+            for (int c = 0; c < NC; ++c) A.s1.out[c][q] = tile[c * RTP + off];
+        });
+    } else {
+        double* dst = (KIND == K_PSI_LAST) ? A.pstar : pick3<double*>(A.io[0], A.io[1], A.io[2], comp);
+        for_tile<AX>(n, R, g0, tb, [&](int l, int m, unsigned q) {
+            const int off = tile_off<L>(l, m, TP);
+            if (KIND == K_LAST) {
+                dst[q] = tile2[off] + tile[off];            // u^{n+1} = u^n + d
+            } else if (KIND == K_PSI_LAST) {
+                const double psi = tile[off];
+                const double pn = tile2[off] + psi;        // Step 3f: p^{n+1/2} = q + psi^{n+1/2}
+                A.p[q] = pn;
+                dst[q] = pn + psi;                         // Step 3a of the next step: p* = p + psi
+            } else {
+                dst[q] = tile[off];
+            }
+        });
     }
 }
 
@@ -421,64 +443,32 @@ __global__ void k_sub(const double* __restrict__ a, const double* __restrict__ b
 // -------------------------------------------------------------------------------
 static size_t smem_limit() { return 220 * 1024; }
 
-// rows per x block: prefer 16, shrink to fit 512 threads and the shared-memory budget
-static int pick_rx(const Ctx* s, int nc)
+static size_t lines_smem(int P, int L, int nc, int R) { return ((size_t)P * P + (size_t)nc * R * tile_pitch(P, L)) * 8; }
+static int tiles_of(int kind, int nc) { return (kind == K_LAST || kind == K_PSI_LAST) ? 2 * nc : nc; }
+
+// lines per block: the largest of {32, 16, 8} whose tile keeps >= 2 blocks per SM
+static int pick_r(const Ctx* s, int L, int nc)
 {
-    for (int R = 16; R >= 1; R /= 2) {
-        if (R * s->P > 512) continue;
-        const size_t sm = ((size_t)s->P * s->P + s->P + (size_t)nc * R * (s->n + 1) + (size_t)4 * nc * s->P * R) * 8;
-        if (sm <= smem_limit()) return R;
-    }
-    return 1;
+    for (int R = 32; R >= 8; R /= 2)
+        if (lines_smem(s->P, L, nc, R) <= 100 * 1024) return R;
+    return 8;
 }
 
-static int pick_ryz(const Ctx* s, int nc)
+template <int L, int KIND, int DIM, int AX, int NC>
+static cudaError_t go_lines(Ctx* s, int sys, const LArgs& a, int ncomp_grid)
 {
-    int R = (nc > 1 ? 256 : 512) / s->P;
-    if (R > 32) R = 32;
-    if (R < 1) R = 1;
-    return R;
-}
-
-// components solved jointly per thread: keep the register arrays x[NCB][L] small
-template <int L, int NC, int LIM>
-struct Ncb { static constexpr int value = (L * NC <= LIM) ? NC : 1; };
-
-template <int L, int OP, int DIM>
-static cudaError_t go_x(Ctx* s, int sys, const S1Args& a1, const XArgs& xa)
-{
-    constexpr int NC = (OP == XOP_S1) ? DIM : 1;
-    constexpr int NCB = Ncb<L, NC, 36>::value;
-    const int R = pick_rx(s, NC);
-    auto kern = k_line_x<L, OP, DIM, NCB>;
-    const size_t sm = ((size_t)s->P * s->P + s->P + (size_t)NC * R * (s->n + 1) + (size_t)4 * NCB * s->P * R) * 8;
+    constexpr int MINB = (KIND == K_S1 || L >= 24) ? 2 : 4;
+    auto kern = k_lines<L, KIND, DIM, AX, NC, MINB>;
+    const int R = pick_r(s, L, tiles_of(KIND, NC));
+    const size_t sm = lines_smem(s->P, L, tiles_of(KIND, NC), R);
     static bool attr_set = false;   // per instantiation
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_limit());
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    dim3 grid((unsigned)((s->n + R - 1) / R), (unsigned)(s->dim == 3 ? s->n : 1));
-    kern<<<grid, R * s->P, sm, s->stream>>>(s->hcoef[sys], s->sinv + sys, (int)s->n, R, a1, xa);
-    s->launches++;
-    return cudaGetLastError();
-}
-
-template <int L, int NC, int OP, int DIM, int AX>
-static cudaError_t go_yz(Ctx* s, int sys, const YArgs& a)
-{
-    constexpr int NCB = Ncb<L, NC, 24>::value;
-    const int R = pick_ryz(s, NCB);
-    auto kern = k_line_yz<L, NCB, OP, DIM, AX>;
-    const size_t sm = ((size_t)s->P * s->P + s->P + (size_t)4 * NCB * s->P * R) * 8;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_limit());
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
-    dim3 grid((unsigned)((s->n + R - 1) / R), (unsigned)(s->dim == 3 ? s->n : 1), (unsigned)(NC / NCB));
-    kern<<<grid, R * s->P, sm, s->stream>>>(s->hcoef[sys], s->sinv + sys, (int)s->n, R, a);
+    dim3 grid((unsigned)((s->n + R - 1) / R), (unsigned)((DIM == 3) ? s->n : 1), (unsigned)ncomp_grid);
+    kern<<<grid, 256, sm, s->stream>>>(s->hcoef[sys], s->sinv + sys, (int)s->n, R, a);
     s->launches++;
     return cudaGetLastError();
 }
@@ -497,90 +487,81 @@ static cudaError_t go_yz(Ctx* s, int sys, const YArgs& a)
         default: return cudaErrorInvalidValue;           \
     }
 
-template <int OP>
-static cudaError_t go_x_dim(Ctx* s, int sys, const S1Args& a1, const XArgs& xa)
-{
-    if (s->dim == 3) { IBGM_DISPATCH_L(s->L, (go_x<LL, OP, 3>(s, sys, a1, xa))) }
-    IBGM_DISPATCH_L(s->L, (go_x<LL, OP, 2>(s, sys, a1, xa)))
-}
-
-// NC3/NC2: components of the pass in 3D/2D; axis 1 or 2
-template <int NC3, int NC2, int OP>
-static cudaError_t go_yz_dim(Ctx* s, int sys, int axis, const YArgs& a)
+// one component per block (blockIdx.z), any axis
+template <int KIND>
+static cudaError_t go_axis(Ctx* s, int sys, int axis, const LArgs& a, int ncomp)
 {
     if (s->dim == 3) {
-        if (axis == 2) { IBGM_DISPATCH_L(s->L, (go_yz<LL, NC3, OP, 3, 2>(s, sys, a))) }
-        IBGM_DISPATCH_L(s->L, (go_yz<LL, NC3, OP, 3, 1>(s, sys, a)))
+        if (axis == 0) { IBGM_DISPATCH_L(s->L, (go_lines<LL, KIND, 3, 0, 1>(s, sys, a, ncomp))) }
+        if (axis == 1) { IBGM_DISPATCH_L(s->L, (go_lines<LL, KIND, 3, 1, 1>(s, sys, a, ncomp))) }
+        IBGM_DISPATCH_L(s->L, (go_lines<LL, KIND, 3, 2, 1>(s, sys, a, ncomp)))
     }
-    IBGM_DISPATCH_L(s->L, (go_yz<LL, NC2, OP, 2, 1>(s, sys, a)))
+    if (axis == 0) { IBGM_DISPATCH_L(s->L, (go_lines<LL, KIND, 2, 0, 1>(s, sys, a, ncomp))) }
+    IBGM_DISPATCH_L(s->L, (go_lines<LL, KIND, 2, 1, 1>(s, sys, a, ncomp)))
 }
 
 cudaError_t launch_s1_x(Ctx* s, int first_step)
 {
-    S1Args a{};
+    LArgs a{};
+    S1Args& b = a.s1;
     for (int c = 0; c < 3; ++c) {
-        a.u[c] = s->u[c]; a.G[c] = s->nprev[c]; a.nadv[c] = s->nadv[c]; a.out[c] = s->st[c];
+        b.u[c] = s->u[c]; b.G[c] = s->nprev[c]; b.nadv[c] = s->nadv[c]; b.out[c] = s->st[c];
     }
-    a.pstar = s->pstar;
-    a.dt = s->dt; a.inv_rho = 1.0 / s->rho; a.mu = s->mu; a.invh = 1.0 / s->h;
-    a.a1 = first_step ? 1.0 : 1.5;
-    a.first = first_step; a.advection = s->advection;
-    XArgs xa{};
-    return go_x_dim<XOP_S1>(s, SYS_VISC, a, xa);
+    b.pstar = s->pstar;
+    b.dt = s->dt; b.inv_rho = 1.0 / s->rho; b.mu = s->mu; b.invh = 1.0 / s->h;
+    b.a1 = first_step ? 1.0 : 1.5;
+    b.first = first_step; b.advection = s->advection;
+    if (s->dim == 3) { IBGM_DISPATCH_L(s->L, (go_lines<LL, K_S1, 3, 0, 3>(s, SYS_VISC, a, 1))) }
+    IBGM_DISPATCH_L(s->L, (go_lines<LL, K_S1, 2, 0, 2>(s, SYS_VISC, a, 1)))
 }
 
 cudaError_t launch_sweep_mid(Ctx* s, int axis)
 {
-    YArgs a{};
+    LArgs a{};
     for (int c = 0; c < 3; ++c) a.io[c] = s->st[c];
-    return go_yz_dim<3, 2, YOP_MID>(s, SYS_VISC, axis, a);
+    return go_axis<K_MID>(s, SYS_VISC, axis, a, s->dim);
 }
 
 cudaError_t launch_sweep_last(Ctx* s, int axis)
 {
-    YArgs a{};
+    LArgs a{};
     for (int c = 0; c < 3; ++c) { a.io[c] = s->st[c]; a.un[c] = s->u[c]; }
-    return go_yz_dim<3, 2, YOP_LAST>(s, SYS_VISC, axis, a);
+    return go_axis<K_LAST>(s, SYS_VISC, axis, a, s->dim);
 }
 
 cudaError_t launch_div_psi_first(Ctx* s, int axis)
 {
-    YArgs a{};
-    a.io[0] = s->pstar;
+    LArgs a{};
+    a.io[0] = a.io[1] = a.io[2] = s->pstar;
     for (int c = 0; c < 3; ++c) { a.un[c] = s->u[c]; a.unew[c] = s->st[c]; }
     a.p = s->p;
     a.neg_rho_dt = -s->rho / s->dt;
     a.chimu_half = 0.5 * s->chi * s->mu;
     a.invh = 1.0 / s->h;
-    return go_yz_dim<1, 1, YOP_DIVPSI>(s, SYS_PSI, axis, a);
+    if (axis == 0) return cudaErrorInvalidValue;
+    return go_axis<K_DIVPSI>(s, SYS_PSI, axis, a, 1);
 }
 
 cudaError_t launch_psi_mid(Ctx* s, int axis)
 {
-    YArgs a{};
-    a.io[0] = s->pstar;
-    return go_yz_dim<1, 1, YOP_MID>(s, SYS_PSI, axis, a);
+    LArgs a{};
+    a.io[0] = a.io[1] = a.io[2] = s->pstar;
+    return go_axis<K_MID>(s, SYS_PSI, axis, a, 1);
 }
 
 cudaError_t launch_psi_last_x(Ctx* s)
 {
-    S1Args a1{};
-    XArgs xa{};
-    xa.in = s->pstar; xa.out = s->pstar; xa.p = s->p;
-    return go_x_dim<XOP_PSI_LAST>(s, SYS_PSI, a1, xa);
+    LArgs a{};
+    a.pstar = s->pstar;
+    a.p = s->p;
+    return go_axis<K_PSI_LAST>(s, SYS_PSI, 0, a, 1);
 }
 
 cudaError_t launch_line_solve(Ctx* s, int axis, int sys, double* data)
 {
-    if (axis == 0) {
-        S1Args a1{};
-        XArgs xa{};
-        xa.in = data; xa.out = data;
-        return go_x_dim<XOP_USER>(s, sys, a1, xa);
-    }
-    YArgs a{};
-    a.io[0] = data;
-    return go_yz_dim<1, 1, YOP_MID>(s, sys, axis, a);
+    LArgs a{};
+    a.io[0] = a.io[1] = a.io[2] = data;
+    return go_axis<K_USER>(s, sys, axis, a, 1);
 }
 
 cudaError_t launch_sub(Ctx* s, const double* a, const double* b, double* out)
