@@ -33,9 +33,8 @@ UNIT = "grid-point updates/s"
 # algorithmic HBM bytes per grid cell of each phase:
 # doubles each phase must read + write once, x 8 B.
 ALG_DOUBLES = {
-    3: {"s1_rhs_xsweep": 17, "visc_y": 9, "visc_z": 9, "div": 9, "psi_z": 2, "psi_y": 2, "psi_x_p": 4,
-        "zero_f": 3},
-    2: {"s1_rhs_xsweep": 12, "visc_y": 6, "div": 7, "psi_y": 2, "psi_x_p": 4, "zero_f": 2},
+    3: {"s1_rhs_xsweep": 13, "sweep_y": 6, "sweep_z": 9, "div_psi_first": 9, "psi_y": 2, "psi_x_p": 4},
+    2: {"s1_rhs_xsweep": 9, "sweep_y": 6, "div_psi_first": 7, "psi_x_p": 4},
 }
 
 
