@@ -154,7 +154,9 @@ int ib_get_stats(ib_ctx* ctx, int64_t* kernel_launches, int64_t* steps_done);
 
 /* Debug flags: bit 0 keeps the spread force f^{n+1/2} as a separate field so that
  * ib_get_aux can return it (costs one extra atomic per spread contribution and a
- * clear per step).  Off by default. */
+ * clear per step).  Bits 1-2 select the spreading method: 0 automatic (per-point
+ * atomics below 3e5 points, brick-binned above), 1 per-point atomics, 2 brick-binned.
+ * Off / automatic by default. */
 int ib_set_debug(ib_ctx* ctx, int32_t flags);
 
 /* Turn per-phase CUDA-event timing on (1) or off (0).  While on, ib_step records an

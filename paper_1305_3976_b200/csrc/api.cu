@@ -148,10 +148,20 @@ static bool choose_segmentation(int64_t n, int* L, int* P)
     return false;
 }
 
+static void drop_graphs(Ctx* s)
+{
+    for (int k = 0; k < 2; ++k) {
+        if (s->gvalid[k]) cudaGraphExecDestroy(s->gexec[k]);
+        s->gvalid[k] = false;
+    }
+}
+
 static void free_lagrangian(Ctx* s)
 {
     cudaFree(s->X); cudaFree(s->Xh); cudaFree(s->Uprev); cudaFree(s->F); cudaFree(s->wgt);
     cudaFree(s->csr_ptr); cudaFree(s->csr_nbr); cudaFree(s->csr_kappa); cudaFree(s->csr_rest);
+    cudaFree(s->bin_bid); cudaFree(s->bin_sorted);
+    s->bin_bid = s->bin_sorted = nullptr;
     s->X = s->Xh = s->Uprev = s->F = s->wgt = nullptr;
     s->csr_ptr = s->csr_nbr = nullptr;
     s->csr_kappa = s->csr_rest = nullptr;
@@ -207,6 +217,7 @@ int ib_create(const ib_grid* grid, double nu, double rho, double dt, const ib_op
     s->advection = o.advection;
     s->device = o.device;
     s->L = L; s->P = P;
+    s->use_graphs = true;
     *out = c;
 
     CKC(cudaSetDevice(o.device));
@@ -234,6 +245,18 @@ int ib_create(const ib_grid* grid, double nu, double rho, double dt, const ib_op
     CKC(cudaMemsetAsync(s->p, 0, fb, s->stream));
     CKC(cudaMemsetAsync(s->pstar, 0, fb, s->stream));
     CKC(cudaMalloc(&s->d_flag, sizeof(int)));
+    // brick grid for the binned spread: 8^3 cells (3D) / 16^2 (2D)
+    {
+        const int B = (s->dim == 3) ? 4 : 8;     // kBrick3 / kBrick2 in ib.cu
+        s->nb = (int)((s->n + B - 1) / B);
+        s->nbricks = (s->dim == 3) ? (int64_t)s->nb * s->nb * s->nb : (int64_t)s->nb * s->nb;
+        CKC(cudaMalloc(&s->bin_count, sizeof(int) * s->nbricks));
+        CKC(cudaMalloc(&s->bin_start, sizeof(int) * s->nbricks));
+        CKC(cudaMalloc(&s->bin_cursor, sizeof(int) * s->nbricks));
+        CKC(cudaMalloc(&s->bin_list, sizeof(int) * s->nbricks));
+        CKC(cudaMalloc(&s->bin_nlist, sizeof(int)));
+        CKC(cudaMalloc(&s->bin_partial, sizeof(int) * ((s->nbricks + 1023) / 1024 + 1)));
+    }
     CKC(cudaMalloc(&s->sinv, sizeof(SchurInv) * SYS_COUNT));
     SchurInv hs[SYS_COUNT];
     // viscous Douglas sweeps: (1 - kap delta) with kap = mu dt / (2 rho h^2)
@@ -286,6 +309,7 @@ int ib_set_boundary(ib_ctx* c, int64_t npts, const double* X, int64_t nedges, co
         if (edges[2 * e] < 0 || edges[2 * e] >= npts || edges[2 * e + 1] < 0 || edges[2 * e + 1] >= npts)
             return fail(IB_EINVAL, "edge %lld references a point out of range", (long long)e);
     CKC(cudaStreamSynchronize(s->stream));
+    drop_graphs(s);
     free_lagrangian(s);
     s->step = 0;
     if (npts == 0) return IB_OK;
@@ -314,6 +338,8 @@ int ib_set_boundary(ib_ctx* c, int64_t npts, const double* X, int64_t nedges, co
     CKC(cudaMalloc(&s->F, pb));
     CKC(cudaMalloc(&s->wgt, npts * sizeof(double)));
     CKC(cudaMalloc(&s->csr_ptr, (npts + 1) * sizeof(int32_t)));
+    CKC(cudaMalloc(&s->bin_bid, npts * sizeof(int)));
+    CKC(cudaMalloc(&s->bin_sorted, npts * sizeof(int)));
     const size_t ne2 = (size_t)(2 * nedges > 0 ? 2 * nedges : 1);
     CKC(cudaMalloc(&s->csr_nbr, ne2 * sizeof(int32_t)));
     CKC(cudaMalloc(&s->csr_kappa, ne2 * sizeof(double)));
@@ -383,15 +409,70 @@ static cudaError_t clear3(Ctx* s, double* const* f)
         }                                                                        \
     } while (0)
 
+static int enqueue_step(Ctx* s, int first);
+
+static void swap_state(Ctx* s)
+{
+    for (int q = 0; q < s->dim; ++q) {
+        std::swap(s->u[q], s->st[q]);
+        std::swap(s->nadv[q], s->nprev[q]);
+    }
+    s->parity ^= 1;
+}
+
 int ib_step(ib_ctx* c, int64_t nsteps)
 {
     if (!c) return fail(IB_EINVAL, "null context");
     Ctx* s = &c->s;
     if (!s->fields_set) return fail(IB_ESTATE, "ib_step before ib_set_fields");
     if (nsteps < 0) return fail(IB_EINVAL, "nsteps < 0");
-    const int d = s->dim;
     for (int64_t t = 0; t < nsteps; ++t) {
         const int first = (s->step == 0);
+        if (!first && !s->profiling && s->use_graphs && !s->debug_keep_f) {
+            // replay the captured regular step for the current pointer parity
+            const int par = s->parity;
+            if (!s->gvalid[par]) {
+                cudaGraph_t g;
+                const int64_t l0 = s->launches;
+                CKC(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal));
+                const int rc = enqueue_step(s, 0);
+                cudaError_t ce = cudaStreamEndCapture(s->stream, &g);
+                if (rc != IB_OK) return rc;
+                CKC(ce);
+                CKC(cudaGraphInstantiate(&s->gexec[par], g, 0));
+                cudaGraphDestroy(g);
+                s->gvalid[par] = true;
+                s->glaunches[par] = s->launches - l0;
+                s->launches = l0;
+            }
+            CKC(cudaGraphLaunch(s->gexec[par], s->stream));
+            s->launches += s->glaunches[par];
+        } else {
+            const int rc = enqueue_step(s, first);
+            if (rc != IB_OK) return rc;
+        }
+        swap_state(s);
+        s->step++;
+        if (s->profiling) {
+            CKC(cudaStreamSynchronize(s->stream));
+            for (int ph = 0; ph < IB_NPHASES; ++ph) {
+                if (!s->ph_pending[ph]) continue;
+                float ms = 0.f;
+                CKC(cudaEventElapsedTime(&ms, s->ev[ph][0], s->ev[ph][1]));
+                s->ph_ms[ph] += ms;
+                s->ph_cnt[ph] += 1;
+                s->ph_pending[ph] = false;
+            }
+        }
+    }
+    return IB_OK;
+}
+
+// all device work of one time step (Steps 1a-3f), enqueued on the context's stream
+static int enqueue_step(Ctx* s, int first)
+{
+    const int d = s->dim;
+    {
         // n = 0: no N(u^{-1}); the history G starts as 0 + (2/rho) f
         if (first) PHASE(IB_PH_CLEAR, clear3(s, s->nprev));
         if (s->debug_keep_f && s->npts > 0) PHASE(IB_PH_CLEAR, clear3(s, s->f));
@@ -414,22 +495,6 @@ int ib_step(ib_ctx* c, int64_t nsteps)
         PHASE(IB_PH_DIVPSI, launch_div_psi_first(s, d - 1));
         if (d == 3) PHASE(IB_PH_PSI_Y, launch_psi_mid(s, 1));
         PHASE(IB_PH_PSI_X, launch_psi_last_x(s));
-        for (int q = 0; q < d; ++q) {
-            std::swap(s->u[q], s->st[q]);
-            std::swap(s->nadv[q], s->nprev[q]);
-        }
-        s->step++;
-        if (s->profiling) {
-            CKC(cudaStreamSynchronize(s->stream));
-            for (int ph = 0; ph < IB_NPHASES; ++ph) {
-                if (!s->ph_pending[ph]) continue;
-                float ms = 0.f;
-                CKC(cudaEventElapsedTime(&ms, s->ev[ph][0], s->ev[ph][1]));
-                s->ph_ms[ph] += ms;
-                s->ph_cnt[ph] += 1;
-                s->ph_pending[ph] = false;
-            }
-        }
     }
     return IB_OK;
 }
@@ -446,7 +511,9 @@ int ib_set_debug(ib_ctx* c, int32_t flags)
             CKC(cudaMemsetAsync(s->f[q], 0, fb, s->stream));
         }
     }
+    drop_graphs(s);
     s->debug_keep_f = keep;
+    s->spread_mode = (flags >> 1) & 3;   // bits 1-2: spread method (0 auto, 1 direct, 2 brick)
     return IB_OK;
 }
 
@@ -565,10 +632,13 @@ int ib_destroy(ib_ctx* c)
     if (!c) return IB_OK;
     Ctx* s = &c->s;
     if (s->stream) cudaStreamSynchronize(s->stream);
+    drop_graphs(s);
     for (int q = 0; q < 3; ++q) {
         cudaFree(s->u[q]); cudaFree(s->st[q]); cudaFree(s->nadv[q]); cudaFree(s->nprev[q]); cudaFree(s->f[q]);
     }
     cudaFree(s->p); cudaFree(s->pstar); cudaFree(s->tmp); cudaFree(s->sinv); cudaFree(s->d_flag);
+    cudaFree(s->bin_count); cudaFree(s->bin_start); cudaFree(s->bin_cursor); cudaFree(s->bin_list);
+    cudaFree(s->bin_nlist); cudaFree(s->bin_partial);
     free_lagrangian(s);
     if (s->ev_made)
         for (int ph = 0; ph < IB_NPHASES; ++ph) { cudaEventDestroy(s->ev[ph][0]); cudaEventDestroy(s->ev[ph][1]); }

@@ -65,11 +65,22 @@ struct Ctx {
     double* csr_kappa;                // [2*nedges]
     double* csr_rest;                 // [2*nedges]
     int has_rest;
+    // brick binning of the points for the spread (Step 2b)
+    int nb;                           // bricks per axis
+    int64_t nbricks;
+    int *bin_bid, *bin_count, *bin_start, *bin_cursor, *bin_list, *bin_nlist, *bin_sorted, *bin_partial;
     int debug_keep_f;                 // ib_set_debug: also accumulate f for ib_get_aux
+    int spread_mode;                  // 0 auto, 1 direct atomics, 2 brick-binned (ib_set_debug bits 1-2)
     int64_t step;                     // steps completed since set_fields/set_boundary
     bool fields_set;
     int64_t launches;
     int* d_flag;                      // device flag for finiteness checks
+    // CUDA graphs of one regular step, one per pointer parity (u <-> st, N <-> G swaps)
+    int parity;
+    bool use_graphs;
+    cudaGraphExec_t gexec[2];
+    bool gvalid[2];
+    int64_t glaunches[2];             // kernels per captured step
     // per-phase profiling (ib_set_profiling)
     int profiling;
     cudaEvent_t ev[IB_NPHASES][2];

@@ -200,8 +200,9 @@ class Context:
     def check_finite(self):
         _ck(lib().ib_check_finite(self._h))
 
-    def set_debug(self, keep_f: bool):
-        _ck(lib().ib_set_debug(self._h, int(keep_f)))
+    def set_debug(self, keep_f: bool, spread_mode: int = 0):
+        """keep_f: keep f^{n+1/2} for aux(); spread_mode: 0 auto, 1 per-point atomics, 2 brick-binned."""
+        _ck(lib().ib_set_debug(self._h, int(keep_f) | (int(spread_mode) << 1)))
 
     def set_profiling(self, on: bool):
         _ck(lib().ib_set_profiling(self._h, int(on)))

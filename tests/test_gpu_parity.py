@@ -81,14 +81,16 @@ def test_line_solve_full_size_sampled_3d_384():
 
 # ------------------------------------------------------------------ one step, per stage
 @pytest.mark.parametrize("cfg,over", [(0, {}), (1, dict(n=64, pts=256)), (3, dict(n=32, nodes=2000)),
-                                      (4, dict(n=48, nodes=1500))])
-def test_one_step_stage_parity(cfg, over):
-    """After one step: X^{n+1/2}, F^{n+1/2}, spread f, N(u^n), then u, p, psi, X."""
+                                      (4, dict(n=48, nodes=1500)), (2, dict(n=128, pts=512))])
+@pytest.mark.parametrize("spread_mode", [1, 2])
+def test_one_step_stage_parity(cfg, over, spread_mode):
+    """After one step: X^{n+1/2}, F^{n+1/2}, spread f, N(u^n), then u, p, psi, X -- with
+    both spreading methods (per-point atomics, brick-binned)."""
     from paper_1305_3976_b200 import inputs
     pr = inputs.config(cfg, **over)
     o = _oracle_for(pr)
     g = _gpu_for(pr)
-    g.set_debug(True)          # keep f^{n+1/2} as a separate field for this comparison
+    g.set_debug(True, spread_mode)   # keep f^{n+1/2} as a separate field for this comparison
     o.step(1)
     g.step(1)
     ao, ag = o.aux(), g.aux()
@@ -108,15 +110,18 @@ def test_one_step_stage_parity(cfg, over):
 
 
 # ------------------------------------------------------------------ 10 steps, configs
-@pytest.mark.parametrize("cfg,over", [(0, {}), (1, {}), (2, {}), (3, {}), (4, dict(n=96, nodes=4000)),
-                                      (2, dict(n=128, pts=256, kernel=1))])
-def test_ten_step_parity(cfg, over):
+@pytest.mark.parametrize("cfg,over,mode", [(0, {}, 0), (1, {}, 0), (2, {}, 0), (3, {}, 0), (3, {}, 2),
+                                           (4, dict(n=96, nodes=4000), 0), (4, dict(n=96, nodes=4000), 2),
+                                           (2, dict(n=128, pts=256, kernel=1), 0)])
+def test_ten_step_parity(cfg, over, mode):
     """End-to-end bar of the north_star: rel L_inf <= 1e-9 on u, p and X after 10 steps.
-    Configs 0-3 at full size; config 4 at reduced N here (full size sampled below)."""
+    Configs 0-3 at full size; config 4 at reduced N here (full size sampled below);
+    mode 2 forces the brick-binned spread."""
     from paper_1305_3976_b200 import inputs
     pr = inputs.config(cfg, **over)
     o = _oracle_for(pr)
     g = _gpu_for(pr)
+    g.set_debug(False, mode)
     o.step(10)
     g.step(10)
     fo, fg = o.fields(), g.fields()

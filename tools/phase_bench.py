@@ -13,6 +13,9 @@ ALG = {3: {"s1_rhs_xsweep": 13, "sweep_y": 6, "sweep_z": 9, "div_psi_first": 9, 
        2: {"s1_rhs_xsweep": 9, "sweep_y": 6, "div_psi_first": 7, "psi_x_p": 4}}
 
 
+MODE = int(os.environ.get("SPREAD_MODE", "0"))
+
+
 def run(cfg, steps=50, **over):
     t0 = time.time()
     pr = inputs.config(cfg, **over)
@@ -20,6 +23,7 @@ def run(cfg, steps=50, **over):
     st = torch.cuda.Stream()
     torch.cuda.set_stream(st)
     ctx = ibgm.from_problem(pr, stream=st.cuda_stream)
+    ctx.set_debug(False, MODE)
     ctx.step(5)
     ctx.sync()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -32,7 +36,7 @@ def run(cfg, steps=50, **over):
     ctx.step(steps)
     ph = ctx.phase_times()
     ctx.close()
-    out = {"cfg": cfg, "over": over, "n": pr.n, "dim": pr.dim, "npts": pr.npts, "ms_per_step": round(ms, 4),
+    out = {"cfg": cfg, "mode": MODE, "over": over, "n": pr.n, "dim": pr.dim, "npts": pr.npts, "ms_per_step": round(ms, 4),
            "updates_per_s": pr.ncell / (ms * 1e-3), "gen_s": round(tg, 1)}
     tot = 0
     for k, (t, c) in ph.items():
