@@ -9,8 +9,9 @@ case); see DESIGN.md "Measurement".  One "step" = one full IB-GM time step
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C]
 
-Prints ONE JSON line on rank 0.  value = N^3 * steps * ranks / (max over ranks of the
-device time of the K timed steps).  Inputs (17 resident fp64 fields, ~285 MB at 128^3)
+Prints ONE JSON line on rank 0.  value = N^d * steps / (max over ranks of the device
+time of the K timed steps).  With N GPUs (torchrun) the same grid is cut into N
+z-slabs, one per rank, over NCCL (strong scaling).  Inputs (17 resident fp64 fields, ~285 MB at 128^3)
 are larger than the 126 MB L2, so no explicit L2 flush is done between steps.
 """
 from __future__ import annotations
@@ -127,6 +128,19 @@ def dist_env():
     return rank, world, local
 
 
+def max_over_ranks(x: float) -> float:
+    """Max of a per-rank scalar over all ranks (the slowest rank's time); identity
+    without a process group.  Uses a CUDA tensor on NCCL, a CPU tensor on gloo."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(x)
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def cpu_baseline(cfg, steps=2):
     """The oracle as it stands, single-threaded, on a bounded sample: `steps` full
     time steps of the same workload (after one untimed step)."""
@@ -195,7 +209,15 @@ def main():
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     assert stream.cuda_stream != 0
-    ctx = ibgm.from_problem(pr, device=local, stream=stream.cuda_stream)
+    if world > 1:
+        # z-slab decomposition over the ranks: NCCL transport, the
+        # unique id broadcast over the process group
+        nccl_id = ibgm.share_nccl_id()
+        ctx = ibgm.from_problem(pr, device=local, stream=stream.cuda_stream, nranks=world, rank=rank,
+                                nccl_id=nccl_id)
+    else:
+        ctx = ibgm.from_problem(pr, device=local, stream=stream.cuda_stream)
+    ncl = pr.ncell // world          # cells this rank holds
 
     def barrier():
         if world > 1:
@@ -219,13 +241,10 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize()
     barrier()
-    ms = e0.elapsed_time(e1)
+    ms = max_over_ranks(e0.elapsed_time(e1))
     launches = ctx.stats()["kernel_launches"] - l0
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
-    updates = float(pr.ncell) * args.steps * world
+    # every step updates the whole N^d grid (each rank its slab): strong scaling
+    updates = float(pr.ncell) * args.steps
     value = updates / (ms * 1e-3)
 
     # --- timed region B: the same K steps with per-phase event pairs (roofline attribution)
@@ -238,16 +257,16 @@ def main():
     tot_ph = sum(v[0] for v in ph.values())
     dom = max((k for k in ph if k in ALG_DOUBLES[dim]), key=lambda k: ph[k][0])
     dom_ms = ph[dom][0] / ph[dom][1]
-    alg = ALG_DOUBLES[dim][dom] * 8 * pr.ncell
+    alg = ALG_DOUBLES[dim][dom] * 8 * ncl
     peak, peak_src = measured_peaks()
     achieved = alg / (dom_ms * 1e-3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", f"traffic_cfg{args.config}.json")
     if os.path.exists(tpath):
         traffic = json.load(open(tpath)).get(dom)
-    step_alg = sum(ALG_DOUBLES[dim][k] for k in ALG_DOUBLES[dim] if k in ph) * 8 * pr.ncell
+    step_alg = sum(ALG_DOUBLES[dim][k] for k in ALG_DOUBLES[dim] if k in ph) * 8 * ncl
     phases = {k: {"ms": round(v[0] / v[1], 5), "share": round(v[0] / tot_ph, 4),
-                  "alg_gbs": (round(ALG_DOUBLES[dim][k] * 8 * pr.ncell / (v[0] / v[1] * 1e-3) / 1e9, 1)
+                  "alg_gbs": (round(ALG_DOUBLES[dim][k] * 8 * ncl / (v[0] / v[1] * 1e-3) / 1e9, 1)
                               if k in ALG_DOUBLES[dim] else None)} for k, v in ph.items()}
 
     # --- e2e through the public API with pinned host buffers
@@ -268,14 +287,10 @@ def main():
             ctx.get_fields_into(hu[0], hu[1], hu[2] if dim == 3 else None, hp, hX)  # D2H of the result
         f1.record(stream)
         torch.cuda.synchronize()
-        ems = f0.elapsed_time(f1)
-        if world > 1:
-            t = torch.tensor([ems], device="cuda")
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            ems = float(t.item())
-        e2e = {"value": float(pr.ncell) * ke * world / (ems * 1e-3), "unit": UNIT,
+        ems = max_over_ranks(f0.elapsed_time(f1))
+        e2e = {"value": float(pr.ncell) * ke / (ems * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": (dim + 1) * pr.ncell * 8,
-               "d2h_bytes_per_step": (dim + 1) * pr.ncell * 8 + pr.npts * dim * 8,
+               "d2h_bytes_per_step": (dim + 1) * pr.ncell * 8 + world * pr.npts * dim * 8,
                "steps": ke, "note": "per step: ib_set_fields (H2D u,v,[w],p from pinned) + ib_step(1) + "
                                     "ib_get_fields (D2H u,v,[w],p,X to pinned)"}
 
@@ -287,11 +302,11 @@ def main():
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "weak" if world > 1 else "strong", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": f"configs[{args.config}]", "grid": f"{n}^{dim}", "ib_points": pr.npts,
                        "ib_edges": int(pr.edges.shape[0]), "mu": pr.mu, "rho": pr.rho, "dt": pr.dt,
-                       "delta_kernel": "cos4", "parallelism": "single-gpu" if world == 1 else f"replicas{world}",
+                       "delta_kernel": "cos4", "parallelism": "single-gpu" if world == 1 else f"zslab{world}-nccl",
                        "l2": "inputs larger than L2 (17 resident fp64 fields), no flush"},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,

@@ -23,8 +23,19 @@
  *   - Device memory and the CUDA stream are owned by the context (unless a stream
  *     is passed in ib_options.stream); all device work of a call is ordered on that
  *     stream.  Calls on one context are not thread-safe.
- *   - With nranks > 1 (z-slab decomposition, not available in this build: returns
- *     IB_EINVAL) field arrays would be the rank's local slab.
+ *   - Z-slab decomposition (nranks > 1): the grid is cut along its
+ *     last axis (z in 3D, y in 2D) into nranks slabs of nz = N/nranks planes; rank r
+ *     owns global planes [r nz, (r+1) nz) (ib_slab_range).  Lines along the cut axis
+ *     are solved by the paper's Schur-complement splitting across ranks
+ *     (PAPER.md:1025-1276); halos move by NCCL.  Lagrangian arrays
+ *     are replicated and always global.  Field arrays are:
+ *       transport IB_TRANSPORT_NCCL    the rank's LOCAL slab, N^{d-1} * nz doubles
+ *                                      (same x-fastest layout, planes z0 .. z0+nz-1);
+ *       transport IB_TRANSPORT_EMULATE the GLOBAL N^d field: the context holds all
+ *                                      nranks slabs on one GPU and runs the same
+ *                                      per-slab kernels and exchanges (copies) in the
+ *                                      same order -- the single-GPU test vehicle of
+ *                                      the decomposition.
  */
 #ifndef IBGM_H
 #define IBGM_H
@@ -39,10 +50,13 @@ extern "C" {
 #define IB_EINVAL (-1)      /* invalid argument (dim, N, dt, rho, nu, chi, edge index ...) */
 #define IB_ESTATE (-2)      /* ib_step before ib_set_fields                                  */
 #define IB_ECUDA (-3)       /* a CUDA runtime call failed (message names it)                  */
-#define IB_ENCCL (-4)       /* reserved: NCCL failure (multi-GPU build)                       */
+#define IB_ENCCL (-4)       /* NCCL could not be loaded or an NCCL call failed                */
 #define IB_ENONFINITE (-5)  /* NaN/Inf detected in the state by ib_check_finite               */
 #define IB_EDOMAIN (-6)     /* reserved: IB point left the rank's slab + halo                 */
 #define IB_ENOMEM (-7)      /* device allocation failed                                       */
+
+#define IB_TRANSPORT_NCCL 0     /* one slab per process, one process per GPU (nranks > 1) */
+#define IB_TRANSPORT_EMULATE 1  /* all nranks slabs in this context, one GPU               */
 
 #define IB_DELTA_COS4 0     /* phi(r) = (1 + cos(pi r/2))/4, |r| < 2: BASELINE.json configs */
 #define IB_DELTA_PESKIN4 1  /* the paper's kernel, eq. (discretedelta)    */
@@ -64,8 +78,13 @@ typedef struct {
                           0: Stokes mode (closed-form tests)                            */
     int32_t device;    /* CUDA ordinal, default 0                                       */
     void* stream;      /* cudaStream_t to order all work on, or NULL (own stream)       */
-    int32_t rank;      /* z-slab rank (must be 0 in this build)                         */
-    int32_t nranks;    /* number of z-slabs (must be 1 in this build)                   */
+    int32_t rank;      /* z-slab rank in [0, nranks) (NCCL transport; 0 otherwise)     */
+    int32_t nranks;    /* number of z-slabs, default 1 (no decomposition); N % nranks
+                          == 0 and N/nranks >= 2                                        */
+    int32_t transport; /* IB_TRANSPORT_NCCL (default) | IB_TRANSPORT_EMULATE            */
+    const void* nccl_id; /* NCCL transport, nranks > 1: the 128-byte unique id that rank 0
+                          obtained from ib_nccl_unique_id and shared with every rank
+                          (e.g. a torch.distributed broadcast); read during ib_create */
 } ib_options;
 
 /* Fill *opt with the defaults listed above. */
@@ -74,8 +93,11 @@ void ib_default_options(ib_options* opt);
 /* Create a context for the grid with kinematic viscosity nu = mu/rho, density rho
  * and time step dt (epsilon = dt).  Allocates every device
  * buffer and precomputes the line-solver factors.  *out receives the context.
+ * With nranks > 1 and the NCCL transport every rank calls ib_create collectively
+ * (ncclCommInitRank on device `device`).
  * Errors: IB_EINVAL (dim not 2/3, N unsupported, H != 1, dt <= 0, rho <= 0, nu < 0,
- * chi not in (0,1], nranks != 1), IB_ECUDA, IB_ENOMEM. */
+ * chi not in (0,1], N % nranks != 0, N/nranks < 2, rank out of range, NCCL transport
+ * without nccl_id), IB_ENCCL, IB_ECUDA, IB_ENOMEM. */
 int ib_create(const ib_grid* grid, double nu, double rho, double dt, const ib_options* opt,
               ib_ctx** out);
 
@@ -129,7 +151,10 @@ int ib_get_aux(ib_ctx* ctx, double* fu, double* fv, double* fw, double* nu, doub
  * along `axis` (0 = x, 1 = y, 2 = z) solve  c x_{i-1} + a x_i + c x_{i+1} = d_i
  * (indices mod N) with a = 1 + 2 kappa, c = -kappa, and write x (N^d, may alias d).
  * Uses the same kernels, segmentation and mean correction as ib_step.  Host buffers.
- * Errors: IB_EINVAL (kappa < 0, axis >= dim). */
+ * On a z-slab context, d and x follow the field convention above and `axis` must be
+ * the cut axis (dim-1): the lines are solved with the cross-rank Schur splitting
+ * (collective across ranks with the NCCL transport).
+ * Errors: IB_EINVAL (kappa < 0, axis >= dim, slab context and axis != dim-1). */
 int ib_line_solve(ib_ctx* ctx, int32_t axis, double kappa, const double* d, double* x);
 
 /* Device-side finiteness check of u, p and X; IB_ENONFINITE if any NaN/Inf. */
@@ -166,6 +191,16 @@ int ib_set_profiling(ib_ctx* ctx, int32_t on);
 
 /* Accumulated milliseconds and launch counts per phase (arrays of IB_NPHASES). */
 int ib_get_phase_times(ib_ctx* ctx, double* ms, int64_t* count);
+
+/* Write a fresh 128-byte NCCL unique id into out[128] (call on rank 0 only, then
+ * share it).  Loads NCCL at run time (the copy already in the process if any).
+ * Needs no GPU.  Errors: IB_EINVAL (null), IB_ENCCL (NCCL missing or failed). */
+int ib_nccl_unique_id(void* out);
+
+/* Global first plane z0 and depth nz of rank `rank`'s slab of an N-cell axis cut into
+ * nranks slabs (z0 = rank N/nranks, nz = N/nranks).  Host-only arithmetic.
+ * Errors: IB_EINVAL (N % nranks != 0, N/nranks < 2, rank out of range). */
+int ib_slab_range(int64_t n, int32_t nranks, int32_t rank, int64_t* z0, int64_t* nz);
 
 /* Release every device buffer, the stream (if owned) and the context. */
 int ib_destroy(ib_ctx* ctx);

@@ -48,51 +48,54 @@ namespace ibgm {
 // and the interface equations give the periodic P x P Schur matrix
 //   S_pp = a - b c (h_m + g_1),  S_{p,p-1} = -c^2 g_m,  S_{p,p+1} = -b^2 h_1
 // (PAPER.md:1192-1219 specialised to constant-coefficient lines).
-void make_line_coef(LineCoef* C, SchurInv* SI, int64_t N, int L, double c_, double a_, double b_, int mean_fix)
+struct SchurF {
+    int m, P;
+    std::vector<long double> inv, cp, g, h, sinv, colsum;
+    long double gsum, hsum;
+};
+
+static void schur_factors(int64_t N, int L, long double c, long double a, long double b, SchurF* F)
 {
-    memset(C, 0, sizeof(*C));
-    memset(SI, 0, sizeof(*SI));
-    const long double c = c_, a = a_, b = b_;
     const int m = L - 1;
     const int P = (int)(N / L);
-    C->c = c_; C->a = a_; C->b = b_;
-    C->L = L; C->P = P; C->N = (int)N; C->mean_fix = mean_fix;
-    C->inv_rowsum = (double)(1.0L / (a + b + c));
-    long double den[kMaxL], cp[kMaxL];
-    den[0] = a;
-    cp[0] = b / den[0];
-    for (int i = 1; i < m; ++i) {
-        den[i] = a - c * cp[i - 1];
-        cp[i] = b / den[i];
+    F->m = m;
+    F->P = P;
+    F->inv.assign(m, 0.0L); F->cp.assign(m, 0.0L); F->g.assign(m, 0.0L); F->h.assign(m, 0.0L);
+    std::vector<long double> den(m > 0 ? m : 1), cp(m > 0 ? m : 1);
+    if (m > 0) {
+        den[0] = a;
+        cp[0] = b / den[0];
+        for (int i = 1; i < m; ++i) {
+            den[i] = a - c * cp[i - 1];
+            cp[i] = b / den[i];
+        }
     }
     for (int i = 0; i < m; ++i) {
-        C->inv[i] = (double)(1.0L / den[i]);
-        C->cp[i] = (double)cp[i];
+        F->inv[i] = 1.0L / den[i];
+        F->cp[i] = cp[i];
     }
-    auto solveB = [&](const long double* d, long double* x) {
-        long double dp[kMaxL];
+    auto solveB = [&](const std::vector<long double>& d, std::vector<long double>& x) {
+        std::vector<long double> dp(m);
         dp[0] = d[0] / den[0];
         for (int i = 1; i < m; ++i) dp[i] = (d[i] - c * dp[i - 1]) / den[i];
         x[m - 1] = dp[m - 1];
         for (int i = m - 2; i >= 0; --i) x[i] = dp[i] - cp[i] * x[i + 1];
     };
-    long double e1[kMaxL] = {0}, em[kMaxL] = {0}, g[kMaxL], h[kMaxL];
-    e1[0] = 1.0L;
-    em[m - 1] = 1.0L;
-    solveB(e1, g);
-    solveB(em, h);
-    long double gs = 0.0L, hs = 0.0L;
-    for (int i = 0; i < m; ++i) {
-        C->g[i] = (double)g[i];
-        C->h[i] = (double)h[i];
-        gs += g[i];
-        hs += h[i];
+    long double g1 = 0.0L, gm = 0.0L, h1 = 0.0L, hm = 0.0L;
+    F->gsum = F->hsum = 0.0L;
+    if (m > 0) {
+        std::vector<long double> e1(m, 0.0L), em(m, 0.0L);
+        e1[0] = 1.0L;
+        em[m - 1] = 1.0L;
+        solveB(e1, F->g);
+        solveB(em, F->h);
+        for (int i = 0; i < m; ++i) { F->gsum += F->g[i]; F->hsum += F->h[i]; }
+        g1 = F->g[0]; gm = F->g[m - 1]; h1 = F->h[0]; hm = F->h[m - 1];
     }
-    C->gsum = (double)gs;
-    C->hsum = (double)hs;
-    const long double s0 = a - b * c * (h[m - 1] + g[0]);
-    const long double sm = -c * c * g[m - 1];
-    const long double sp = -b * b * h[0];
+    // m = 0 (one unknown per part): the parts couple directly, S = tridiag(c, a, b)
+    const long double s0 = (m > 0) ? a - b * c * (hm + g1) : a;
+    const long double sm = (m > 0) ? -c * c * gm : c;
+    const long double sp = (m > 0) ? -b * b * h1 : b;
     std::vector<long double> S((size_t)P * P, 0.0L), I((size_t)P * P, 0.0L);
     for (int p = 0; p < P; ++p) {
         S[(size_t)p * P + p] += s0;
@@ -100,7 +103,7 @@ void make_line_coef(LineCoef* C, SchurInv* SI, int64_t N, int L, double c_, doub
         S[(size_t)p * P + (p + 1) % P] += sp;
         I[(size_t)p * P + p] = 1.0L;
     }
-    // Gauss-Jordan with partial pivoting (P <= 32)
+    // Gauss-Jordan with partial pivoting (P is small)
     for (int col = 0; col < P; ++col) {
         int piv = col;
         for (int r = col + 1; r < P; ++r)
@@ -125,12 +128,56 @@ void make_line_coef(LineCoef* C, SchurInv* SI, int64_t N, int L, double c_, doub
             }
         }
     }
-    for (int i = 0; i < P * P; ++i) SI->sinv[i] = (double)I[i];
-    for (int q = 0; q < P; ++q) {
-        long double cs = 0.0L;
-        for (int p = 0; p < P; ++p) cs += I[(size_t)p * P + q];
-        SI->colsum[q] = (double)cs;
+    F->sinv = I;
+    F->colsum.assign(P, 0.0L);
+    for (int q = 0; q < P; ++q)
+        for (int p = 0; p < P; ++p) F->colsum[q] += I[(size_t)p * P + q];
+}
+
+void make_line_coef(LineCoef* C, SchurInv* SI, int64_t N, int L, double c_, double a_, double b_, int mean_fix)
+{
+    memset(C, 0, sizeof(*C));
+    memset(SI, 0, sizeof(*SI));
+    SchurF F;
+    schur_factors(N, L, c_, a_, b_, &F);
+    C->c = c_; C->a = a_; C->b = b_;
+    C->L = L; C->P = F.P; C->N = (int)N; C->mean_fix = mean_fix;
+    C->inv_rowsum = (double)(1.0L / ((long double)a_ + b_ + c_));
+    for (int i = 0; i < F.m; ++i) {
+        C->inv[i] = (double)F.inv[i];
+        C->cp[i] = (double)F.cp[i];
+        C->g[i] = (double)F.g[i];
+        C->h[i] = (double)F.h[i];
     }
+    C->gsum = (double)F.gsum;
+    C->hsum = (double)F.hsum;
+    for (int i = 0; i < F.P * F.P; ++i) SI->sinv[i] = (double)F.sinv[i];
+    for (int q = 0; q < F.P; ++q) SI->colsum[q] = (double)F.colsum[q];
+}
+
+// Slab coefficient block (layout in ibgm_internal.cuh): the same factors for a line of
+// N = P nz unknowns cut at the slab boundaries (part = slab).
+static std::vector<double> slab_coef_block(int64_t N, int nz, double c, double a, double b, int mf)
+{
+    SchurF F;
+    schur_factors(N, nz, c, a, b, &F);
+    const int m = F.m, P = F.P;
+    std::vector<double> v(SC_HDR + 4 * m + P * P + P, 0.0);
+    v[SC_C] = c; v[SC_A] = a; v[SC_B] = b;
+    v[SC_INVROW] = (double)(1.0L / ((long double)a + b + c));
+    v[SC_GSUM] = (double)F.gsum;
+    v[SC_HSUM] = (double)F.hsum;
+    v[SC_N] = (double)N;
+    v[SC_MF] = mf;
+    for (int i = 0; i < m; ++i) {
+        v[SC_HDR + i] = (double)F.inv[i];
+        v[SC_HDR + m + i] = (double)F.cp[i];
+        v[SC_HDR + 2 * m + i] = (double)F.g[i];
+        v[SC_HDR + 3 * m + i] = (double)F.h[i];
+    }
+    for (int i = 0; i < P * P; ++i) v[SC_HDR + 4 * m + i] = (double)F.sinv[i];
+    for (int q = 0; q < P; ++q) v[SC_HDR + 4 * m + P * P + q] = (double)F.colsum[q];
+    return v;
 }
 
 }  // namespace ibgm
@@ -166,6 +213,87 @@ static void free_lagrangian(Ctx* s)
     s->csr_ptr = s->csr_nbr = nullptr;
     s->csr_kappa = s->csr_rest = nullptr;
     s->npts = s->nedges = 0;
+    if (s->grp) {
+        cudaFree(s->grp->Upart); cudaFree(s->grp->Ured);
+        s->grp->Upart = s->grp->Ured = nullptr;
+        s->grp->ucap = 0;
+    }
+}
+
+// one field of the local extent (plus a halo plane on each side on a z-slab), zeroed;
+// the pointer addresses plane 0
+static cudaError_t field_alloc(Ctx* s, double** out)
+{
+    const int halo = s->wrap ? 0 : 1;
+    const size_t bytes = (size_t)(s->nl + 2 * halo) * s->plane * sizeof(double);
+    double* b = nullptr;
+    cudaError_t e = cudaMalloc(&b, bytes);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(b, 0, bytes, s->stream);
+    *out = b + s->hoff;
+    return e;
+}
+
+static void field_free(Ctx* s, double*& p)
+{
+    if (p) cudaFree(p - s->hoff);
+    p = nullptr;
+}
+
+static cudaError_t alloc_fields(Ctx* s)
+{
+    cudaError_t e;
+    for (int q = 0; q < s->dim; ++q) {
+        if ((e = field_alloc(s, &s->u[q])) != cudaSuccess) return e;
+        if ((e = field_alloc(s, &s->st[q])) != cudaSuccess) return e;
+        if ((e = field_alloc(s, &s->nadv[q])) != cudaSuccess) return e;
+        if ((e = field_alloc(s, &s->nprev[q])) != cudaSuccess) return e;
+    }
+    if ((e = field_alloc(s, &s->p)) != cudaSuccess) return e;
+    if ((e = field_alloc(s, &s->pstar)) != cudaSuccess) return e;
+    if ((e = field_alloc(s, &s->tmp)) != cudaSuccess) return e;
+    return cudaMalloc(&s->d_flag, sizeof(int));
+}
+
+static void free_fields(Ctx* s)
+{
+    for (int q = 0; q < 3; ++q) {
+        field_free(s, s->u[q]); field_free(s, s->st[q]); field_free(s, s->nadv[q]);
+        field_free(s, s->nprev[q]); field_free(s, s->f[q]);
+    }
+    field_free(s, s->p); field_free(s, s->pstar); field_free(s, s->tmp);
+    cudaFree(s->d_flag);
+    s->d_flag = nullptr;
+}
+
+// local slabs of a context: itself on a single GPU, else the group's slabs
+static int nslabs(Ctx* s) { return s->grp ? s->grp->nloc : 1; }
+static Ctx* slab_at(Ctx* s, int r) { return s->grp ? s->grp->slab[r] : s; }
+
+// host-array offset (doubles) of a slab's plane 0 in the fields passed through the API
+static size_t host_off(Ctx* s, Ctx* sl)
+{
+    return (s->grp && s->grp->transport == IB_TRANSPORT_EMULATE) ? (size_t)(sl->z0 * sl->plane) : 0;
+}
+
+static int64_t total_launches(Ctx* s)
+{
+    int64_t t = s->launches;
+    if (s->grp)
+        for (int r = 0; r < s->grp->nloc; ++r) t += s->grp->slab[r]->launches;
+    return t;
+}
+
+static int upload_coef(Ctx* s, int sys, double c, double a, double b, int mf)
+{
+    Group* G = s->grp;
+    std::vector<double> v = slab_coef_block(s->n, (int)(s->n / G->P), c, a, b, mf);
+    if (G->coef[sys]) cudaFree(G->coef[sys]);
+    G->coef[sys] = nullptr;
+    CKC(cudaMalloc(&G->coef[sys], v.size() * sizeof(double)));
+    CKC(cudaMemcpyAsync(G->coef[sys], v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice, s->stream));
+    CKC(cudaStreamSynchronize(s->stream));
+    return IB_OK;
 }
 
 extern "C" {
@@ -180,9 +308,34 @@ void ib_default_options(ib_options* o)
     o->stream = nullptr;
     o->rank = 0;
     o->nranks = 1;
+    o->transport = IB_TRANSPORT_NCCL;
+    o->nccl_id = nullptr;
 }
 
 const char* ib_last_error(void) { return g_err.c_str(); }
+
+int ib_slab_range(int64_t n, int32_t nranks, int32_t rank, int64_t* z0, int64_t* nz)
+{
+    if (nranks < 1 || nranks > kMaxRanks) return fail(IB_EINVAL, "nranks must be in [1, %d]", kMaxRanks);
+    if (rank < 0 || rank >= nranks) return fail(IB_EINVAL, "rank %d out of [0, %d)", rank, nranks);
+    if (n % nranks != 0) return fail(IB_EINVAL, "N = %lld is not divisible by nranks = %d", (long long)n, nranks);
+    if (n / nranks < 2) return fail(IB_EINVAL, "slab depth N/nranks = %lld < 2", (long long)(n / nranks));
+    if (z0) *z0 = (n / nranks) * rank;
+    if (nz) *nz = n / nranks;
+    return IB_OK;
+}
+
+int ib_nccl_unique_id(void* out)
+{
+    if (!out) return fail(IB_EINVAL, "null argument");
+    const char* e = nccl_load();
+    if (e) return fail(IB_ENCCL, "%s", e);
+    NcclUid id;
+    const int rc = nccl_unique_id(&id);
+    if (rc != 0) return fail(IB_ENCCL, "ncclGetUniqueId: %s", nccl_error_string(rc));
+    memcpy(out, &id, sizeof(id));
+    return IB_OK;
+}
 
 int ib_create(const ib_grid* grid, double nu, double rho, double dt, const ib_options* opt, ib_ctx** out)
 {
@@ -195,10 +348,21 @@ int ib_create(const ib_grid* grid, double nu, double rho, double dt, const ib_op
     if (grid->H != 1.0) return fail(IB_EINVAL, "H must be 1 (the psi operator is literal, DESIGN.md R2)");
     if (!(dt > 0) || !(rho > 0) || !(nu >= 0)) return fail(IB_EINVAL, "need dt > 0, rho > 0, nu >= 0");
     if (!(o.chi > 0 && o.chi <= 1)) return fail(IB_EINVAL, "chi must be in (0, 1]");
-    if (o.nranks != 1 || o.rank != 0) return fail(IB_EINVAL, "this build runs one rank per process (nranks = 1)");
     if (o.kernel != IB_DELTA_COS4 && o.kernel != IB_DELTA_PESKIN4) return fail(IB_EINVAL, "unknown delta kernel");
-    int L, P;
-    if (!choose_segmentation(grid->n, &L, &P))
+    if (o.transport != IB_TRANSPORT_NCCL && o.transport != IB_TRANSPORT_EMULATE)
+        return fail(IB_EINVAL, "unknown transport %d", o.transport);
+    const int P = o.nranks;
+    if (P < 1) return fail(IB_EINVAL, "nranks must be >= 1");
+    if (P > 1) {
+        const int rc = ib_slab_range(grid->n, P, o.transport == IB_TRANSPORT_NCCL ? o.rank : 0, nullptr, nullptr);
+        if (rc != IB_OK) return rc;
+        if (o.transport == IB_TRANSPORT_EMULATE && o.rank != 0) return fail(IB_EINVAL, "EMULATE transport: rank must be 0");
+        if (o.transport == IB_TRANSPORT_NCCL && !o.nccl_id) return fail(IB_EINVAL, "NCCL transport needs nccl_id");
+    } else if (o.rank != 0) {
+        return fail(IB_EINVAL, "rank must be 0 when nranks = 1");
+    }
+    int L, Pseg;
+    if (!choose_segmentation(grid->n, &L, &Pseg))
         return fail(IB_EINVAL, "N = %lld has no divisor L in {2,3,4,6,8,12,16,24,32} with N/L <= 32",
                     (long long)grid->n);
 
@@ -208,6 +372,7 @@ int ib_create(const ib_grid* grid, double nu, double rho, double dt, const ib_op
     s->dim = grid->dim;
     s->n = grid->n;
     s->ncell = grid->dim == 3 ? grid->n * grid->n * grid->n : grid->n * grid->n;
+    s->plane = grid->dim == 3 ? grid->n * grid->n : grid->n;
     s->h = 1.0 / (double)grid->n;
     s->rho = rho;
     s->mu = nu * rho;
@@ -216,8 +381,10 @@ int ib_create(const ib_grid* grid, double nu, double rho, double dt, const ib_op
     s->kernel = o.kernel;
     s->advection = o.advection;
     s->device = o.device;
-    s->L = L; s->P = P;
+    s->L = L; s->P = Pseg;
     s->use_graphs = true;
+    s->wrap = 1;
+    s->nl = s->n;
     *out = c;
 
     CKC(cudaSetDevice(o.device));
@@ -227,35 +394,6 @@ int ib_create(const ib_grid* grid, double nu, double rho, double dt, const ib_op
     } else {
         CKC(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
         s->own_stream = true;
-    }
-    const size_t fb = (size_t)s->ncell * sizeof(double);
-    for (int q = 0; q < s->dim; ++q) {
-        CKC(cudaMalloc(&s->u[q], fb));
-        CKC(cudaMalloc(&s->st[q], fb));
-        CKC(cudaMalloc(&s->nadv[q], fb));
-        CKC(cudaMalloc(&s->nprev[q], fb));
-        CKC(cudaMemsetAsync(s->u[q], 0, fb, s->stream));
-        CKC(cudaMemsetAsync(s->st[q], 0, fb, s->stream));
-        CKC(cudaMemsetAsync(s->nadv[q], 0, fb, s->stream));
-        CKC(cudaMemsetAsync(s->nprev[q], 0, fb, s->stream));
-    }
-    CKC(cudaMalloc(&s->p, fb));
-    CKC(cudaMalloc(&s->pstar, fb));
-    CKC(cudaMalloc(&s->tmp, fb));
-    CKC(cudaMemsetAsync(s->p, 0, fb, s->stream));
-    CKC(cudaMemsetAsync(s->pstar, 0, fb, s->stream));
-    CKC(cudaMalloc(&s->d_flag, sizeof(int)));
-    // brick grid for the binned spread: 8^3 cells (3D) / 16^2 (2D)
-    {
-        const int B = (s->dim == 3) ? 4 : 8;     // kBrick3 / kBrick2 in ib.cu
-        s->nb = (int)((s->n + B - 1) / B);
-        s->nbricks = (s->dim == 3) ? (int64_t)s->nb * s->nb * s->nb : (int64_t)s->nb * s->nb;
-        CKC(cudaMalloc(&s->bin_count, sizeof(int) * s->nbricks));
-        CKC(cudaMalloc(&s->bin_start, sizeof(int) * s->nbricks));
-        CKC(cudaMalloc(&s->bin_cursor, sizeof(int) * s->nbricks));
-        CKC(cudaMalloc(&s->bin_list, sizeof(int) * s->nbricks));
-        CKC(cudaMalloc(&s->bin_nlist, sizeof(int)));
-        CKC(cudaMalloc(&s->bin_partial, sizeof(int) * ((s->nbricks + 1023) / 1024 + 1)));
     }
     CKC(cudaMalloc(&s->sinv, sizeof(SchurInv) * SYS_COUNT));
     SchurInv hs[SYS_COUNT];
@@ -268,6 +406,70 @@ int ib_create(const ib_grid* grid, double nu, double rho, double dt, const ib_op
     make_line_coef(&s->hcoef[SYS_PSI], &hs[SYS_PSI], s->n, L, -kp, 1.0 + 2.0 * kp, -kp, 1);
     make_line_coef(&s->hcoef[SYS_USER], &hs[SYS_USER], s->n, L, -kv, 1.0 + 2.0 * kv, -kv, 0);
     CKC(cudaMemcpyAsync(s->sinv, hs, sizeof(SchurInv) * SYS_COUNT, cudaMemcpyHostToDevice, s->stream));
+
+    if (P == 1) {
+        s->nlocal = s->ncell;
+        s->hoff = 0;
+        CKC(alloc_fields(s));
+    } else {
+        // z-slab decomposition: the top context keeps the Lagrangian state; each slab
+        // context holds the fields of nz planes (+ halos) and borrows the stream and the
+        // line factors of the top
+        s->nlocal = 0;
+        CKC(cudaMalloc(&s->d_flag, sizeof(int)));
+        Group* G = new Group();
+        memset(G, 0, sizeof(*G));
+        s->grp = G;
+        G->P = P;
+        G->transport = o.transport;
+        G->rank = (o.transport == IB_TRANSPORT_NCCL) ? o.rank : 0;
+        G->nloc = (o.transport == IB_TRANSPORT_EMULATE) ? P : 1;
+        const int64_t nz = s->n / P;
+        for (int r = 0; r < G->nloc; ++r) {
+            Ctx* sl = new Ctx();
+            memset(sl, 0, sizeof(*sl));
+            sl->dim = s->dim; sl->n = s->n; sl->ncell = s->ncell; sl->plane = s->plane;
+            sl->h = s->h; sl->mu = s->mu; sl->rho = s->rho; sl->dt = s->dt; sl->chi = s->chi;
+            sl->kernel = s->kernel; sl->advection = s->advection; sl->device = s->device;
+            sl->stream = s->stream; sl->own_stream = false;
+            sl->L = L; sl->P = Pseg;
+            sl->sinv = s->sinv;
+            memcpy(sl->hcoef, s->hcoef, sizeof(s->hcoef));
+            sl->rank = (o.transport == IB_TRANSPORT_EMULATE) ? r : o.rank;
+            sl->nl = nz;
+            sl->z0 = nz * sl->rank;
+            sl->wrap = 0;
+            sl->nlocal = nz * s->plane;
+            sl->hoff = s->plane;
+            G->slab[r] = sl;
+            CKC(alloc_fields(sl));
+        }
+        CKC(cudaMalloc(&G->gather, sizeof(double) * (size_t)P * kSlabSlots * s->plane));
+        CKC(cudaMemsetAsync(G->gather, 0, sizeof(double) * (size_t)P * kSlabSlots * s->plane, s->stream));
+        int rc;
+        if ((rc = upload_coef(s, SYS_VISC, -kv, 1.0 + 2.0 * kv, -kv, 0)) != IB_OK) return rc;
+        if ((rc = upload_coef(s, SYS_PSI, -kp, 1.0 + 2.0 * kp, -kp, 1)) != IB_OK) return rc;
+        if (o.transport == IB_TRANSPORT_NCCL) {
+            const char* e = nccl_load();
+            if (e) return fail(IB_ENCCL, "%s", e);
+            NcclUid id;
+            memcpy(&id, o.nccl_id, sizeof(id));
+            const int nr = nccl_comm_init(&G->comm, P, &id, o.rank);
+            if (nr != 0) return fail(IB_ENCCL, "ncclCommInitRank: %s", nccl_error_string(nr));
+        }
+    }
+    // brick grid for the binned spread: 4^3 cells (3D) / 8^2 (2D)
+    {
+        const int B = (s->dim == 3) ? 4 : 8;     // kBrick3 / kBrick2 in ib.cu
+        s->nb = (int)((s->n + B - 1) / B);
+        s->nbricks = (s->dim == 3) ? (int64_t)s->nb * s->nb * s->nb : (int64_t)s->nb * s->nb;
+        CKC(cudaMalloc(&s->bin_count, sizeof(int) * s->nbricks));
+        CKC(cudaMalloc(&s->bin_start, sizeof(int) * s->nbricks));
+        CKC(cudaMalloc(&s->bin_cursor, sizeof(int) * s->nbricks));
+        CKC(cudaMalloc(&s->bin_list, sizeof(int) * s->nbricks));
+        CKC(cudaMalloc(&s->bin_nlist, sizeof(int)));
+        CKC(cudaMalloc(&s->bin_partial, sizeof(int) * ((s->nbricks + 1023) / 1024 + 1)));
+    }
     CKC(cudaStreamSynchronize(s->stream));
     return IB_OK;
 }
@@ -276,19 +478,24 @@ int ib_set_fields(ib_ctx* c, const double* u, const double* v, const double* w, 
 {
     if (!c || !u || !v || (c->s.dim == 3 && !w)) return fail(IB_EINVAL, "null field pointer");
     Ctx* s = &c->s;
-    const size_t fb = (size_t)s->ncell * sizeof(double);
     const double* in[3] = {u, v, w};
-    for (int q = 0; q < s->dim; ++q) {
-        CKC(cudaMemcpyAsync(s->u[q], in[q], fb, cudaMemcpyHostToDevice, s->stream));
-        CKC(cudaMemsetAsync(s->nprev[q], 0, fb, s->stream));
-    }
-    // p^{-1/2} = p (or 0), psi^{-1/2} = 0, so p* = p (R5)
-    if (p) {
-        CKC(cudaMemcpyAsync(s->p, p, fb, cudaMemcpyHostToDevice, s->stream));
-        CKC(cudaMemcpyAsync(s->pstar, p, fb, cudaMemcpyHostToDevice, s->stream));
-    } else {
-        CKC(cudaMemsetAsync(s->p, 0, fb, s->stream));
-        CKC(cudaMemsetAsync(s->pstar, 0, fb, s->stream));
+    for (int r = 0; r < nslabs(s); ++r) {
+        Ctx* sl = slab_at(s, r);
+        const size_t fb = (size_t)sl->nlocal * sizeof(double);
+        const size_t off = host_off(s, sl);
+        const size_t full = (size_t)(sl->nl + (sl->wrap ? 0 : 2)) * sl->plane * sizeof(double);
+        for (int q = 0; q < s->dim; ++q) {
+            CKC(cudaMemcpyAsync(sl->u[q], in[q] + off, fb, cudaMemcpyHostToDevice, s->stream));
+            CKC(cudaMemsetAsync(sl->nprev[q] - sl->hoff, 0, full, s->stream));
+        }
+        // p^{-1/2} = p (or 0), psi^{-1/2} = 0, so p* = p (R5)
+        if (p) {
+            CKC(cudaMemcpyAsync(sl->p, p + off, fb, cudaMemcpyHostToDevice, s->stream));
+            CKC(cudaMemcpyAsync(sl->pstar, p + off, fb, cudaMemcpyHostToDevice, s->stream));
+        } else {
+            CKC(cudaMemsetAsync(sl->p, 0, fb, s->stream));
+            CKC(cudaMemsetAsync(sl->pstar, 0, fb, s->stream));
+        }
     }
     CKC(cudaStreamSynchronize(s->stream));
     s->step = 0;
@@ -355,6 +562,15 @@ int ib_set_boundary(ib_ctx* c, int64_t npts, const double* X, int64_t nedges, co
         CKC(cudaMemcpyAsync(s->csr_kappa, kap.data(), 2 * nedges * sizeof(double), cudaMemcpyHostToDevice, s->stream));
         CKC(cudaMemcpyAsync(s->csr_rest, rst.data(), 2 * nedges * sizeof(double), cudaMemcpyHostToDevice, s->stream));
     }
+    if (s->grp) {
+        Group* G = s->grp;
+        const int64_t cnt = npts * d;
+        const int slots = (G->transport == IB_TRANSPORT_EMULATE) ? G->P : 1;
+        CKC(cudaMalloc(&G->Upart, sizeof(double) * cnt * slots));
+        CKC(cudaMalloc(&G->Ured, sizeof(double) * cnt));
+        CKC(cudaMemsetAsync(G->Upart, 0, sizeof(double) * cnt * slots, s->stream));
+        G->ucap = cnt;
+    }
     CKC(cudaStreamSynchronize(s->stream));
     s->npts = npts;
     s->nedges = nedges;
@@ -390,7 +606,7 @@ int ib_set_fibers(ib_ctx* c, int32_t n_fibers, const int64_t* pts_per_fiber, con
 
 static cudaError_t clear3(Ctx* s, double* const* f)
 {
-    const size_t fb = (size_t)s->ncell * sizeof(double);
+    const size_t fb = (size_t)s->nlocal * sizeof(double);
     for (int q = 0; q < s->dim; ++q) {
         cudaError_t e = cudaMemsetAsync(f[q], 0, fb, s->stream);
         if (e != cudaSuccess) return e;
@@ -409,16 +625,44 @@ static cudaError_t clear3(Ctx* s, double* const* f)
         }                                                                        \
     } while (0)
 
+// a transport call (returns 0 or a cudaError_t / ncclResult_t)
+#define CKG(call)                                                                                   \
+    do {                                                                                            \
+        const int rc_ = (call);                                                                     \
+        if (rc_ != 0) {                                                                             \
+            if (s->grp->transport == IB_TRANSPORT_NCCL)                                             \
+                return fail(IB_ENCCL, "%s: %s (%s:%d)", #call, nccl_error_string(rc_), __FILE__, __LINE__); \
+            return fail(IB_ECUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString((cudaError_t)rc_), __FILE__, \
+                        __LINE__);                                                                  \
+        }                                                                                           \
+    } while (0)
+
+// every local slab
+#define FOR_SLABS(call)                                          \
+    do {                                                         \
+        for (int r_ = 0; r_ < s->grp->nloc; ++r_) {              \
+            Ctx* sl = s->grp->slab[r_];                          \
+            (void)sl;                                            \
+            CKC(call);                                           \
+        }                                                        \
+    } while (0)
+
 static int enqueue_step(Ctx* s, int first);
+static int enqueue_step_slab(Ctx* s, int first);
 
 static void swap_state(Ctx* s)
 {
-    for (int q = 0; q < s->dim; ++q) {
-        std::swap(s->u[q], s->st[q]);
-        std::swap(s->nadv[q], s->nprev[q]);
+    for (int r = 0; r < nslabs(s); ++r) {
+        Ctx* sl = slab_at(s, r);
+        for (int q = 0; q < s->dim; ++q) {
+            std::swap(sl->u[q], sl->st[q]);
+            std::swap(sl->nadv[q], sl->nprev[q]);
+        }
     }
     s->parity ^= 1;
 }
+
+static int enqueue_any(Ctx* s, int first) { return s->grp ? enqueue_step_slab(s, first) : enqueue_step(s, first); }
 
 int ib_step(ib_ctx* c, int64_t nsteps)
 {
@@ -433,22 +677,22 @@ int ib_step(ib_ctx* c, int64_t nsteps)
             const int par = s->parity;
             if (!s->gvalid[par]) {
                 cudaGraph_t g;
-                const int64_t l0 = s->launches;
+                const int64_t l0 = total_launches(s);
                 CKC(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal));
-                const int rc = enqueue_step(s, 0);
+                const int rc = enqueue_any(s, 0);
                 cudaError_t ce = cudaStreamEndCapture(s->stream, &g);
                 if (rc != IB_OK) return rc;
                 CKC(ce);
                 CKC(cudaGraphInstantiate(&s->gexec[par], g, 0));
                 cudaGraphDestroy(g);
                 s->gvalid[par] = true;
-                s->glaunches[par] = s->launches - l0;
-                s->launches = l0;
+                s->glaunches[par] = total_launches(s) - l0;
+                s->launches -= s->glaunches[par];   // captured, not launched
             }
             CKC(cudaGraphLaunch(s->gexec[par], s->stream));
             s->launches += s->glaunches[par];
         } else {
-            const int rc = enqueue_step(s, first);
+            const int rc = enqueue_any(s, first);
             if (rc != IB_OK) return rc;
         }
         swap_state(s);
@@ -499,17 +743,114 @@ static int enqueue_step(Ctx* s, int first)
     return IB_OK;
 }
 
+static double* fld_u0(Ctx* c) { return c->u[0]; }
+static double* fld_u1(Ctx* c) { return c->u[1]; }
+static double* fld_u2(Ctx* c) { return c->u[2]; }
+static double* fld_pstar(Ctx* c) { return c->pstar; }
+static double* fld_st_last2(Ctx* c) { return c->st[1]; }
+static double* fld_st_last3(Ctx* c) { return c->st[2]; }
+
+// The same step on a z-slab decomposition: each phase runs on every local slab, with
+// the exchanges between phases (a12: halos, a13: the cut-axis line solves, and the
+// sum of the partial interpolations).
+static int enqueue_step_slab(Ctx* s, int first)
+{
+    const int d = s->dim;
+    Group* G = s->grp;
+    if (first) FOR_SLABS(clear3(sl, sl->nprev));
+    if (s->debug_keep_f && s->npts > 0) FOR_SLABS(clear3(sl, sl->f));
+    if (s->npts > 0) {
+        if (s->profiling) CKC(cudaEventRecord(s->ev[IB_PH_INTERP][0], s->stream));
+        // Step 1a: each slab interpolates from the nodes it owns; U^n = sum over slabs
+        const int64_t cnt = s->npts * d;
+        for (int r = 0; r < G->nloc; ++r) {
+            double* part = G->Upart + ((G->transport == IB_TRANSPORT_EMULATE) ? (size_t)r * cnt : 0);
+            CKC(slab_interp_part(s, G->slab[r], part));
+        }
+        CKG(group_allreduce_U(G, s, s->stream));
+        // Steps 1b-1c on every rank (identical arithmetic on identical U^n)
+        CKC(slab_evolve(s, G->Ured, first));
+        if (s->profiling) {
+            CKC(cudaEventRecord(s->ev[IB_PH_INTERP][1], s->stream));
+            s->ph_pending[IB_PH_INTERP] = true;
+        }
+        PHASE(IB_PH_FORCE, launch_force(s));
+        if (s->profiling) CKC(cudaEventRecord(s->ev[IB_PH_SPREAD][0], s->stream));
+        FOR_SLABS(slab_spread_part(s, sl));
+        if (s->profiling) {
+            CKC(cudaEventRecord(s->ev[IB_PH_SPREAD][1], s->stream));
+            s->ph_pending[IB_PH_SPREAD] = true;
+        }
+    }
+    if (s->profiling) CKC(cudaEventRecord(s->ev[IB_PH_S1][0], s->stream));
+    // halos for Steps 3a-3b: u (every component) on both sides, p* below
+    {
+        HaloSpec h[4] = {{fld_u0, true, true}, {fld_u1, true, true}, {fld_u2, true, true}, {fld_pstar, true, false}};
+        if (d == 2) h[2] = h[3];
+        CKG(group_halo(G, d + 1, h, s->stream));
+    }
+    FOR_SLABS(launch_s1_x(sl, first));
+    if (s->profiling) {
+        CKC(cudaEventRecord(s->ev[IB_PH_S1][1], s->stream));
+        s->ph_pending[IB_PH_S1] = true;
+    }
+    const int last_ph = (d == 3) ? IB_PH_SWEEP_Z : IB_PH_SWEEP_Y;
+    if (d == 3) {
+        if (s->profiling) CKC(cudaEventRecord(s->ev[IB_PH_SWEEP_Y][0], s->stream));
+        FOR_SLABS(launch_sweep_mid(sl, 1));
+        if (s->profiling) {
+            CKC(cudaEventRecord(s->ev[IB_PH_SWEEP_Y][1], s->stream));
+            s->ph_pending[IB_PH_SWEEP_Y] = true;
+        }
+    }
+    // the last Douglas sweep along the cut axis (distributed Schur solve)
+    if (s->profiling) CKC(cudaEventRecord(s->ev[last_ph][0], s->stream));
+    FOR_SLABS(slab_sweep_last_fwd(sl, G));
+    CKG(group_allgather(G, s->stream));
+    FOR_SLABS(slab_sweep_last_corr(sl, G));
+    if (s->profiling) {
+        CKC(cudaEventRecord(s->ev[last_ph][1], s->stream));
+        s->ph_pending[last_ph] = true;
+    }
+    // Step 3e: D.u^{n+1} needs u^{n+1}_last one plane above
+    if (s->profiling) CKC(cudaEventRecord(s->ev[IB_PH_DIVPSI][0], s->stream));
+    {
+        HaloSpec h[1] = {{d == 3 ? fld_st_last3 : fld_st_last2, false, true}};
+        CKG(group_halo(G, 1, h, s->stream));
+    }
+    FOR_SLABS(slab_divpsi_fwd(sl, G));
+    CKG(group_allgather(G, s->stream));
+    FOR_SLABS(slab_divpsi_corr(sl, G));
+    if (s->profiling) {
+        CKC(cudaEventRecord(s->ev[IB_PH_DIVPSI][1], s->stream));
+        s->ph_pending[IB_PH_DIVPSI] = true;
+    }
+    if (d == 3) {
+        if (s->profiling) CKC(cudaEventRecord(s->ev[IB_PH_PSI_Y][0], s->stream));
+        FOR_SLABS(launch_psi_mid(sl, 1));
+        if (s->profiling) {
+            CKC(cudaEventRecord(s->ev[IB_PH_PSI_Y][1], s->stream));
+            s->ph_pending[IB_PH_PSI_Y] = true;
+        }
+    }
+    if (s->profiling) CKC(cudaEventRecord(s->ev[IB_PH_PSI_X][0], s->stream));
+    FOR_SLABS(launch_psi_last_x(sl));
+    if (s->profiling) {
+        CKC(cudaEventRecord(s->ev[IB_PH_PSI_X][1], s->stream));
+        s->ph_pending[IB_PH_PSI_X] = true;
+    }
+    return IB_OK;
+}
+
 int ib_set_debug(ib_ctx* c, int32_t flags)
 {
     if (!c) return fail(IB_EINVAL, "null context");
     Ctx* s = &c->s;
     const int keep = (flags & 1) != 0;
-    if (keep && !s->f[0]) {
-        const size_t fb = (size_t)s->ncell * sizeof(double);
-        for (int q = 0; q < s->dim; ++q) {
-            CKC(cudaMalloc(&s->f[q], fb));
-            CKC(cudaMemsetAsync(s->f[q], 0, fb, s->stream));
-        }
+    for (int r = 0; r < nslabs(s); ++r) {
+        Ctx* sl = slab_at(s, r);
+        if (keep && !sl->f[0])
+            for (int q = 0; q < s->dim; ++q) CKC(field_alloc(sl, &sl->f[q]));
     }
     drop_graphs(s);
     s->debug_keep_f = keep;
@@ -552,15 +893,19 @@ int ib_get_fields(ib_ctx* c, double* u, double* v, double* w, double* p, double*
 {
     if (!c) return fail(IB_EINVAL, "null context");
     Ctx* s = &c->s;
-    const size_t fb = (size_t)s->ncell * sizeof(double);
     double* out[3] = {u, v, w};
-    for (int q = 0; q < s->dim; ++q)
-        if (out[q]) CKC(cudaMemcpyAsync(out[q], s->u[q], fb, cudaMemcpyDeviceToHost, s->stream));
-    if (p) CKC(cudaMemcpyAsync(p, s->p, fb, cudaMemcpyDeviceToHost, s->stream));
-    if (psi) {
-        // the state keeps p* = p + psi; psi^{n-1/2} = p* - p
-        CKC(launch_sub(s, s->pstar, s->p, s->tmp));
-        CKC(cudaMemcpyAsync(psi, s->tmp, fb, cudaMemcpyDeviceToHost, s->stream));
+    for (int r = 0; r < nslabs(s); ++r) {
+        Ctx* sl = slab_at(s, r);
+        const size_t fb = (size_t)sl->nlocal * sizeof(double);
+        const size_t off = host_off(s, sl);
+        for (int q = 0; q < s->dim; ++q)
+            if (out[q]) CKC(cudaMemcpyAsync(out[q] + off, sl->u[q], fb, cudaMemcpyDeviceToHost, s->stream));
+        if (p) CKC(cudaMemcpyAsync(p + off, sl->p, fb, cudaMemcpyDeviceToHost, s->stream));
+        if (psi) {
+            // the state keeps p* = p + psi; psi^{n-1/2} = p* - p
+            CKC(launch_sub(sl, sl->pstar, sl->p, sl->tmp));
+            CKC(cudaMemcpyAsync(psi + off, sl->tmp, fb, cudaMemcpyDeviceToHost, s->stream));
+        }
     }
     const size_t pb = (size_t)s->npts * s->dim * sizeof(double);
     if (X && pb) CKC(cudaMemcpyAsync(X, s->X, pb, cudaMemcpyDeviceToHost, s->stream));
@@ -574,13 +919,17 @@ int ib_get_aux(ib_ctx* c, double* fu, double* fv, double* fw, double* nu, double
 {
     if (!c) return fail(IB_EINVAL, "null context");
     Ctx* s = &c->s;
-    const size_t fb = (size_t)s->ncell * sizeof(double);
     double* fo[3] = {fu, fv, fw};
     double* no[3] = {nu, nv, nw};
     if ((fu || fv || fw) && !s->debug_keep_f) return fail(IB_ESTATE, "f is only kept with ib_set_debug(ctx, 1)");
-    for (int q = 0; q < s->dim; ++q) {
-        if (fo[q]) CKC(cudaMemcpyAsync(fo[q], s->f[q], fb, cudaMemcpyDeviceToHost, s->stream));
-        if (no[q]) CKC(cudaMemcpyAsync(no[q], s->nprev[q], fb, cudaMemcpyDeviceToHost, s->stream));
+    for (int r = 0; r < nslabs(s); ++r) {
+        Ctx* sl = slab_at(s, r);
+        const size_t fb = (size_t)sl->nlocal * sizeof(double);
+        const size_t off = host_off(s, sl);
+        for (int q = 0; q < s->dim; ++q) {
+            if (fo[q]) CKC(cudaMemcpyAsync(fo[q] + off, sl->f[q], fb, cudaMemcpyDeviceToHost, s->stream));
+            if (no[q]) CKC(cudaMemcpyAsync(no[q] + off, sl->nprev[q], fb, cudaMemcpyDeviceToHost, s->stream));
+        }
     }
     const size_t pb = (size_t)s->npts * s->dim * sizeof(double);
     if (F && pb) CKC(cudaMemcpyAsync(F, s->F, pb, cudaMemcpyDeviceToHost, s->stream));
@@ -595,9 +944,30 @@ int ib_line_solve(ib_ctx* c, int32_t axis, double kappa, const double* d, double
     Ctx* s = &c->s;
     if (axis < 0 || axis >= s->dim) return fail(IB_EINVAL, "axis %d out of range", axis);
     if (!(kappa >= 0)) return fail(IB_EINVAL, "kappa must be >= 0");
-    static SchurInv hs;
     // the exact mean correction is applied to the ill-conditioned systems (kappa > 1, R16)
-    make_line_coef(&s->hcoef[SYS_USER], &hs, s->n, s->L, -kappa, 1.0 + 2.0 * kappa, -kappa, kappa > 1.0 ? 1 : 0);
+    const int mf = kappa > 1.0 ? 1 : 0;
+    if (s->grp) {
+        if (axis != s->dim - 1) return fail(IB_EINVAL, "on a z-slab context ib_line_solve solves along the cut axis");
+        const int rc = upload_coef(s, SYS_USER, -kappa, 1.0 + 2.0 * kappa, -kappa, mf);
+        if (rc != IB_OK) return rc;
+        for (int r = 0; r < nslabs(s); ++r) {
+            Ctx* sl = slab_at(s, r);
+            CKC(cudaMemcpyAsync(sl->tmp, d + host_off(s, sl), (size_t)sl->nlocal * sizeof(double),
+                                cudaMemcpyHostToDevice, s->stream));
+        }
+        FOR_SLABS(slab_user_fwd(sl, s->grp, sl->tmp, mf));
+        CKG(group_allgather(s->grp, s->stream));
+        FOR_SLABS(slab_user_corr(sl, s->grp, sl->tmp, mf));
+        for (int r = 0; r < nslabs(s); ++r) {
+            Ctx* sl = slab_at(s, r);
+            CKC(cudaMemcpyAsync(x + host_off(s, sl), sl->tmp, (size_t)sl->nlocal * sizeof(double),
+                                cudaMemcpyDeviceToHost, s->stream));
+        }
+        CKC(cudaStreamSynchronize(s->stream));
+        return IB_OK;
+    }
+    static SchurInv hs;
+    make_line_coef(&s->hcoef[SYS_USER], &hs, s->n, s->L, -kappa, 1.0 + 2.0 * kappa, -kappa, mf);
     const size_t fb = (size_t)s->ncell * sizeof(double);
     CKC(cudaMemcpyAsync(s->sinv + SYS_USER, &hs, sizeof(SchurInv), cudaMemcpyHostToDevice, s->stream));
     CKC(cudaMemcpyAsync(s->tmp, d, fb, cudaMemcpyHostToDevice, s->stream));
@@ -611,18 +981,25 @@ int ib_check_finite(ib_ctx* c)
 {
     if (!c) return fail(IB_EINVAL, "null context");
     Ctx* s = &c->s;
-    CKC(launch_check_finite(s));
-    int flag = 0;
-    CKC(cudaMemcpyAsync(&flag, s->d_flag, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
-    CKC(cudaStreamSynchronize(s->stream));
-    if (flag) return fail(IB_ENONFINITE, "non-finite value in u, p or X after %lld steps", (long long)s->step);
+    int bad = 0;
+    // fields per slab; X (and, on a single GPU, the fields) on the top context, whose
+    // nlocal is 0 when it holds no fields
+    for (int r = 0; r <= (s->grp ? s->grp->nloc : 0); ++r) {
+        Ctx* cc = (s->grp && r < s->grp->nloc) ? s->grp->slab[r] : s;
+        CKC(launch_check_finite(cc));
+        int flag = 0;
+        CKC(cudaMemcpyAsync(&flag, cc->d_flag, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
+        CKC(cudaStreamSynchronize(s->stream));
+        bad |= flag;
+    }
+    if (bad) return fail(IB_ENONFINITE, "non-finite value in u, p or X after %lld steps", (long long)s->step);
     return IB_OK;
 }
 
 int ib_get_stats(ib_ctx* c, int64_t* launches, int64_t* steps)
 {
     if (!c) return fail(IB_EINVAL, "null context");
-    if (launches) *launches = c->s.launches;
+    if (launches) *launches = total_launches(&c->s);
     if (steps) *steps = c->s.step;
     return IB_OK;
 }
@@ -633,13 +1010,27 @@ int ib_destroy(ib_ctx* c)
     Ctx* s = &c->s;
     if (s->stream) cudaStreamSynchronize(s->stream);
     drop_graphs(s);
-    for (int q = 0; q < 3; ++q) {
-        cudaFree(s->u[q]); cudaFree(s->st[q]); cudaFree(s->nadv[q]); cudaFree(s->nprev[q]); cudaFree(s->f[q]);
+    if (s->grp) {
+        Group* G = s->grp;
+        for (int r = 0; r < G->nloc; ++r) {
+            if (!G->slab[r]) continue;
+            free_fields(G->slab[r]);
+            delete G->slab[r];
+        }
+        cudaFree(G->gather);
+        for (int k = 0; k < SYS_COUNT; ++k) cudaFree(G->coef[k]);
+        free_lagrangian(s);
+        nccl_comm_destroy(G->comm);
+        delete G;
+        s->grp = nullptr;
+        cudaFree(s->d_flag);
+    } else {
+        free_fields(s);
+        free_lagrangian(s);
     }
-    cudaFree(s->p); cudaFree(s->pstar); cudaFree(s->tmp); cudaFree(s->sinv); cudaFree(s->d_flag);
+    cudaFree(s->sinv);
     cudaFree(s->bin_count); cudaFree(s->bin_start); cudaFree(s->bin_cursor); cudaFree(s->bin_list);
     cudaFree(s->bin_nlist); cudaFree(s->bin_partial);
-    free_lagrangian(s);
     if (s->ev_made)
         for (int ph = 0; ph < IB_NPHASES; ++ph) { cudaEventDestroy(s->ev[ph][0]); cudaEventDestroy(s->ev[ph][1]); }
     if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);

@@ -152,22 +152,35 @@ struct S1Args {
     int first, advection;
 };
 
-// Row bases of one x-row (j, k) and its y/z neighbours, 32-bit flat offsets.
+// Row bases of one x-row (j, k) and its y/z neighbours, signed 32-bit flat offsets.
+// The last axis (z in 3D, y in 2D) has nl local planes; it wraps periodically on a
+// single GPU (wrap = 1) and, on a z-slab (wrap = 0), reaches the halo planes -1 and nl
+// that the halo exchange filled.
 struct RowB {
-    unsigned r0, ryp, rym, rzp, rzm, rypzm, rymzp;
+    int r0, ryp, rym, rzp, rzm, rypzm, rymzp;
 };
 
+__device__ __forceinline__ int nbr_lo(int k, int nl, int wrap) { return (k == 0) ? (wrap ? nl - 1 : -1) : k - 1; }
+__device__ __forceinline__ int nbr_hi(int k, int nl, int wrap) { return (k == nl - 1) ? (wrap ? 0 : nl) : k + 1; }
+
 template <int DIM>
-__device__ __forceinline__ RowB row_bases(int j, int k, int n)
+__device__ __forceinline__ RowB row_bases(int j, int k, int n, int nl, int wrap)
 {
-    const unsigned N = (unsigned)n, NN = N * N;
-    const unsigned jm = (j == 0) ? n - 1 : j - 1, jp = (j == n - 1) ? 0 : j + 1;
+    const int N = n, NN = n * n;
+    int jm, jp;
+    if (DIM == 2) {
+        jm = nbr_lo(j, nl, wrap);
+        jp = nbr_hi(j, nl, wrap);
+    } else {
+        jm = (j == 0) ? n - 1 : j - 1;
+        jp = (j == n - 1) ? 0 : j + 1;
+    }
     RowB b;
-    unsigned kk = 0, km = 0, kp = 0;
+    int kk = 0, km = 0, kp = 0;
     if (DIM == 3) {
-        kk = NN * (unsigned)k;
-        km = NN * (unsigned)((k == 0) ? n - 1 : k - 1);
-        kp = NN * (unsigned)((k == n - 1) ? 0 : k + 1);
+        kk = NN * k;
+        km = NN * nbr_lo(k, nl, wrap);
+        kp = NN * nbr_hi(k, nl, wrap);
     }
     b.r0 = N * j + kk;
     b.ryp = N * jp + kk;
@@ -187,9 +200,9 @@ __device__ __forceinline__ RowB row_bases(int j, int k, int n)
 template <int DIM>
 __device__ __forceinline__ void s1_cell(const S1Args& A, int i, const RowB& rb, int n, double (&d)[3])
 {
-    const unsigned im = (i == 0) ? n - 1 : i - 1, ip = (i == n - 1) ? 0 : i + 1, ii = (unsigned)i;
+    const int im = (i == 0) ? n - 1 : i - 1, ip = (i == n - 1) ? 0 : i + 1, ii = i;
     // offsets of I, I+e_x, I-e_x, I+e_y, I-e_y, I+e_z, I-e_z  (index 0, 1+2a, 2+2a)
-    unsigned o[7];
+    int o[7];
     o[0] = ii + rb.r0;
     o[1] = ip + rb.r0;
     o[2] = im + rb.r0;
@@ -198,7 +211,7 @@ __device__ __forceinline__ void s1_cell(const S1Args& A, int i, const RowB& rb, 
     o[5] = ii + rb.rzp;
     o[6] = ii + rb.rzm;
     // I + e_m - e_c  (m != c)
-    unsigned mx[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+    int mx[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
     mx[0][1] = ip + rb.rym;
     mx[1][0] = im + rb.ryp;
     if (DIM == 3) {
@@ -266,19 +279,22 @@ struct LArgs {
     double* p;              // DIVPSI: p -> q ; PSI_LAST: q -> p^{n+1/2}
     double* pstar;          // PSI_LAST: psi in, p* out
     double neg_rho_dt, chimu_half, invh;
+    int nl;                 // local planes of the last axis (N, or the slab depth)
+    int wrap;               // 1: the last axis is periodic here; 0: z-slab with halo planes
 };
 
 // Visit every (line l, position m) of the block's tile with coalesced global offsets:
 // consecutive threads take consecutive x.  f(l, m, q) with q the 32-bit flat index.
+// nrow bounds the rows of an x-line tile (the local planes of the last axis in 2D).
 template <int AX, class F>
-__device__ __forceinline__ void for_tile(int n, int R, int g0, unsigned tb, F&& f)
+__device__ __forceinline__ void for_tile(int n, int nrow, int R, int g0, unsigned tb, F&& f)
 {
     const int t = threadIdx.x, T = blockDim.x;
     const unsigned N = (unsigned)n;
     if (AX == 0) {
         if (n >= T) {
             for (int l = 0; l < R; ++l) {
-                if (g0 + l >= n) break;
+                if (g0 + l >= nrow) break;
                 const unsigned rb = N * (unsigned)(g0 + l) + N * N * tb;
                 for (int m = t; m < n; m += T) f(l, m, rb + (unsigned)m);
             }
@@ -286,7 +302,7 @@ __device__ __forceinline__ void for_tile(int n, int R, int g0, unsigned tb, F&& 
             const int rows = T / n;          // rows covered per sweep of the block
             const int l0 = t / n, m = t - l0 * n;
             if (l0 >= rows) return;
-            for (int l = l0; l < R && g0 + l < n; l += rows) f(l, m, (unsigned)m + N * (unsigned)(g0 + l) + N * N * tb);
+            for (int l = l0; l < R && g0 + l < nrow; l += rows) f(l, m, (unsigned)m + N * (unsigned)(g0 + l) + N * N * tb);
         }
     } else {
         const int lg = 31 - __clz(R);        // R is a power of two
@@ -319,12 +335,13 @@ __global__ void __launch_bounds__(256, MINB) k_lines(const LineCoef C, const Sch
     const int g0 = blockIdx.x * R;              // first j (AX = 0) or first i (AX = 1, 2)
     const unsigned tb = blockIdx.y;             // k (AX = 0, 1 in 3D) or j (AX = 2)
     const unsigned RTP = (unsigned)R * TP;
+    const int nrow = (DIM == 2) ? A.nl : n;     // x-line rows (AX = 0)
 
     // ---------------- fill (coalesced: consecutive threads -> consecutive x)
     if (KIND == K_S1) {
         if (n >= T) {
-            for (int l = 0; l < R && g0 + l < n; ++l) {
-                const RowB rb = row_bases<DIM>(g0 + l, (int)tb, n);
+            for (int l = 0; l < R && g0 + l < nrow; ++l) {
+                const RowB rb = row_bases<DIM>(g0 + l, (int)tb, n, A.nl, A.wrap);
                 for (int m = t; m < n; m += T) {
                     double v[3];
                     s1_cell<DIM>(A.s1, m, rb, n, v);
@@ -337,8 +354,8 @@ __global__ void __launch_bounds__(256, MINB) k_lines(const LineCoef C, const Sch
             const int rows = T / n;
             const int l0 = t / n, m = t - l0 * n;
             if (l0 < rows)
-                for (int l = l0; l < R && g0 + l < n; l += rows) {
-                    const RowB rb = row_bases<DIM>(g0 + l, (int)tb, n);
+                for (int l = l0; l < R && g0 + l < nrow; l += rows) {
+                    const RowB rb = row_bases<DIM>(g0 + l, (int)tb, n, A.nl, A.wrap);
                     double v[3];
                     s1_cell<DIM>(A.s1, m, rb, n, v);
                     const int off = tile_off<L>(l, m, TP);
@@ -349,7 +366,7 @@ __global__ void __launch_bounds__(256, MINB) k_lines(const LineCoef C, const Sch
     } else if (KIND == K_DIVPSI) {
         // D.u at each cell for u^{n+1} and u^n
         const unsigned stp[3] = {1u, N, N * N};
-        for_tile<AX>(n, R, g0, tb, [&](int l, int m, unsigned q) {
+        for_tile<AX>(n, nrow, R, g0, tb, [&](int l, int m, unsigned q) {
             // cell coordinates along each axis: i = g0 + l; the line axis coordinate is m
             int ijk[3];
             ijk[0] = g0 + l;
@@ -371,7 +388,7 @@ __global__ void __launch_bounds__(256, MINB) k_lines(const LineCoef C, const Sch
         const double* src = (KIND == K_PSI_LAST) ? A.pstar : pick3<double*>(A.io[0], A.io[1], A.io[2], comp);
         const double* src2 = (KIND == K_LAST) ? pick3<const double*>(A.un[0], A.un[1], A.un[2], comp)
                                               : (KIND == K_PSI_LAST ? A.p : nullptr);
-        for_tile<AX>(n, R, g0, tb, [&](int l, int m, unsigned q) {
+        for_tile<AX>(n, nrow, R, g0, tb, [&](int l, int m, unsigned q) {
             const int off = tile_off<L>(l, m, TP);
             cp_async8(tile + off, src + q);
             if (KIND == K_LAST || KIND == K_PSI_LAST) cp_async8(tile2 + off, src2 + q);
@@ -409,14 +426,14 @@ __global__ void __launch_bounds__(256, MINB) k_lines(const LineCoef C, const Sch
 
     // ---------------- store (coalesced)
     if (KIND == K_S1) {
-        for_tile<AX>(n, R, g0, tb, [&](int l, int m, unsigned q) {
+        for_tile<AX>(n, nrow, R, g0, tb, [&](int l, int m, unsigned q) {
             const int off = tile_off<L>(l, m, TP);
 #pragma unroll
             for (int c = 0; c < NC; ++c) A.s1.out[c][q] = tile[c * RTP + off];
         });
     } else {
         double* dst = (KIND == K_PSI_LAST) ? A.pstar : pick3<double*>(A.io[0], A.io[1], A.io[2], comp);
-        for_tile<AX>(n, R, g0, tb, [&](int l, int m, unsigned q) {
+        for_tile<AX>(n, nrow, R, g0, tb, [&](int l, int m, unsigned q) {
             const int off = tile_off<L>(l, m, TP);
             if (KIND == K_LAST) {
                 dst[q] = tile2[off] + tile[off];            // u^{n+1} = u^n + d
@@ -467,8 +484,14 @@ static cudaError_t go_lines(Ctx* s, int sys, const LArgs& a, int ncomp_grid)
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    dim3 grid((unsigned)((s->n + R - 1) / R), (unsigned)((DIM == 3) ? s->n : 1), (unsigned)ncomp_grid);
-    kern<<<grid, 256, sm, s->stream>>>(s->hcoef[sys], s->sinv + sys, (int)s->n, R, a);
+    // a pass along the last axis needs the whole line on this GPU
+    if (AX == DIM - 1 && !s->wrap) return cudaErrorInvalidValue;
+    LArgs la = a;
+    la.nl = (int)s->nl;
+    la.wrap = s->wrap;
+    const int64_t rows = (AX == 0 && DIM == 2) ? s->nl : s->n;
+    dim3 grid((unsigned)((rows + R - 1) / R), (unsigned)((DIM == 3) ? s->nl : 1), (unsigned)ncomp_grid);
+    kern<<<grid, 256, sm, s->stream>>>(s->hcoef[sys], s->sinv + sys, (int)s->n, R, la);
     s->launches++;
     return cudaGetLastError();
 }
@@ -566,7 +589,7 @@ cudaError_t launch_line_solve(Ctx* s, int axis, int sys, double* data)
 
 cudaError_t launch_sub(Ctx* s, const double* a, const double* b, double* out)
 {
-    k_sub<<<592, 256, 0, s->stream>>>(a, b, out, (size_t)s->ncell);
+    k_sub<<<592, 256, 0, s->stream>>>(a, b, out, (size_t)s->nlocal);
     s->launches++;
     return cudaGetLastError();
 }

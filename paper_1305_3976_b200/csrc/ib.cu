@@ -551,10 +551,10 @@ cudaError_t launch_check_finite(Ctx* s)
     cudaError_t e = cudaMemsetAsync(s->d_flag, 0, sizeof(int), s->stream);
     if (e != cudaSuccess) return e;
     for (int c = 0; c < s->dim; ++c) {
-        k_check_finite<<<592, thr, 0, s->stream>>>(s->u[c], (size_t)s->ncell, s->d_flag);
+        k_check_finite<<<592, thr, 0, s->stream>>>(s->u[c], (size_t)s->nlocal, s->d_flag);
         s->launches++;
     }
-    k_check_finite<<<592, thr, 0, s->stream>>>(s->p, (size_t)s->ncell, s->d_flag);
+    k_check_finite<<<592, thr, 0, s->stream>>>(s->p, (size_t)s->nlocal, s->d_flag);
     s->launches++;
     if (s->npts) {
         k_check_finite<<<592, thr, 0, s->stream>>>(s->X, (size_t)s->npts * s->dim, s->d_flag);

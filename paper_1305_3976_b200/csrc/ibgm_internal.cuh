@@ -38,9 +38,18 @@ struct SchurInv {
 
 enum SysId { SYS_VISC = 0, SYS_PSI = 1, SYS_USER = 2, SYS_COUNT = 3 };
 
+struct Group;
+
 struct Ctx {
     int dim;
     int64_t n, ncell;
+    // local extent: the last axis (z in 3D, y in 2D) has nl planes starting at global
+    // plane z0; nl = n, z0 = 0, wrap = 1 on a single GPU; on a z-slab wrap = 0 and the
+    // fields carry one halo plane on each side (pointers address plane 0, hoff doubles
+    // in from the allocation)
+    int64_t nl, z0, plane, nlocal, hoff;
+    int wrap, rank;
+    Group* grp;                       // z-slab decomposition (nullptr on a single GPU)
     double h, mu, rho, dt, chi;
     int kernel, advection, device;
     cudaStream_t stream;
@@ -89,6 +98,56 @@ struct Ctx {
     int64_t ph_cnt[IB_NPHASES];
     bool ph_pending[IB_NPHASES];
 };
+
+// ---------------------------------------------------------------------------------
+// z-slab decomposition (slab.cu)
+// ---------------------------------------------------------------------------------
+struct NcclUid { char internal[128]; };
+
+// slab coefficient block header (doubles), followed by inv, cp, g, h [m], S^{-1} [P*P],
+// colsum(S^{-1}) [P]
+enum { SC_C = 0, SC_A, SC_B, SC_INVROW, SC_GSUM, SC_HSUM, SC_N, SC_MF, SC_HDR = 8 };
+constexpr int kSlabSlots = 6;         // gather slots per rank: 2 per velocity component / 4 for psi
+constexpr int kMaxRanks = 64;
+
+struct Group {
+    int P;                            // ranks (slabs)
+    int transport;                    // IB_TRANSPORT_EMULATE | IB_TRANSPORT_NCCL
+    int rank;                         // NCCL: this process's rank
+    int nloc;                         // slabs held by this context (P emulated, 1 with NCCL)
+    Ctx* slab[kMaxRanks];
+    double* gather;                   // [P][kSlabSlots][plane]
+    double* Upart;                    // partial interpolation ([P][npts*d] emulated, [npts*d] NCCL)
+    double* Ured;                     // U^n after the sum over ranks
+    int64_t ucap;                     // capacity (points*d) of Upart/Ured
+    double* coef[SYS_COUNT];          // device slab coefficient blocks
+    void* comm;                       // ncclComm_t
+};
+
+struct HaloSpec {
+    double* (*field)(Ctx*);
+    bool up, down;
+};
+
+const char* nccl_load(void);
+int nccl_unique_id(NcclUid* id);
+int nccl_comm_init(void** comm, int nranks, const NcclUid* id, int rank);
+void nccl_comm_destroy(void* comm);
+const char* nccl_error_string(int rc);
+
+cudaError_t slab_sweep_last_fwd(Ctx* s, Group* G);
+cudaError_t slab_sweep_last_corr(Ctx* s, Group* G);
+cudaError_t slab_divpsi_fwd(Ctx* s, Group* G);
+cudaError_t slab_divpsi_corr(Ctx* s, Group* G);
+cudaError_t slab_user_fwd(Ctx* s, Group* G, double* data, int mf);
+cudaError_t slab_user_corr(Ctx* s, Group* G, double* data, int mf);
+cudaError_t slab_interp_part(Ctx* top, Ctx* s, double* Upart);
+cudaError_t slab_sum_slots(Ctx* top, const double* part, int P, double* out);
+cudaError_t slab_evolve(Ctx* top, const double* U, int first);
+cudaError_t slab_spread_part(Ctx* top, Ctx* s);
+int group_halo(Group* G, int nf, const HaloSpec* spec, cudaStream_t st);
+int group_allgather(Group* G, cudaStream_t st);
+int group_allreduce_U(Group* G, Ctx* top, cudaStream_t st);
 
 // host-side precompute (api.cu)
 void make_line_coef(LineCoef* C, SchurInv* S, int64_t N, int L, double c, double a, double b, int mean_fix);

@@ -1,0 +1,620 @@
+// Z-slab decomposition of the IB-GM step, sm_100a, fp64.
+//
+// The grid is cut along its last axis (z in 3D, y in 2D) into P slabs of nz = N/P
+// planes; slab s owns global planes [s nz, (s+1) nz).  Every field keeps one halo plane
+// on each side (planes -1 and nz), which is all the stencils of Steps 3b/3e need
+// (PAPER.md:807-833).  The Lagrangian data is replicated on every rank:
+//   - interpolation (Step 1a): each rank sums the delta-weighted velocities of the grid
+//     nodes it owns; one all-reduce over ranks forms U^n, then every rank evolves all
+//     points identically (Steps 1b-1c);
+//   - spreading (Step 2b): each rank spreads every point into the nodes it owns only,
+//     so no reverse halo sum is needed.
+// Lines along x and y lie inside a slab and use the single-GPU line kernels.  Lines
+// along the cut axis are solved with the paper's Schur-complement splitting across
+// ranks: slab s is part s of every line -- its first plane is the
+// interface unknown y_s and planes 1..nz-1 are the interior block B_s.  Each rank
+// solves B_s f*_s = d_s (Thomas, one thread per line, coalesced across x), publishes
+// per line the scalars the reduced system needs, an all-gather replaces the paper's
+// gather to the master rank (every rank then holds the whole reduced right-hand side),
+// and each rank applies the precomputed S^{-1} to get its own y_s, y_{s+1} and
+// corrects x_s = f*_s - B_s^{-1} E_s y.
+//
+// Two transports move the halo planes, the reduced system and the partial U:
+//   EMULATE  P virtual slabs in one context on one GPU (device-to-device copies and a
+//            shared gather buffer) -- the same kernels in the same order, used to test
+//            the decomposition at the parity bar with a single GPU;
+//   NCCL     one slab per process (one process per GPU), grouped ncclSend/ncclRecv for
+//            halos, ncclAllGather for the reduced system, ncclAllReduce for U.  NCCL is
+//            loaded at run time (the copy torch already loaded if present).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+#include "ibgm_internal.cuh"
+
+namespace ibgm {
+
+// ------------------------------------------------------------------------------------
+// NCCL, loaded at run time (minimal ABI: ncclUniqueId is 128 bytes, enums are int)
+// ------------------------------------------------------------------------------------
+struct NcclApi {
+    bool ok = false;
+    int (*GetUniqueId)(NcclUid*) = nullptr;
+    int (*CommInitRank)(void**, int, NcclUid, int) = nullptr;
+    int (*CommDestroy)(void*) = nullptr;
+    int (*AllReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+    int (*AllGather)(const void*, void*, size_t, int, void*, cudaStream_t) = nullptr;
+    int (*Send)(const void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+    int (*Recv)(void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+    int (*GroupStart)() = nullptr;
+    int (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(int) = nullptr;
+};
+constexpr int kNcclDouble = 8, kNcclSum = 0;
+
+static NcclApi g_nccl;
+
+const char* nccl_load(void)
+{
+    static char err[256] = "";
+    if (g_nccl.ok) return nullptr;
+    void* h = nullptr;
+    const char* env = getenv("IBGM_NCCL_LIB");
+    if (env && *env) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);   // the copy torch loaded
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+        snprintf(err, sizeof(err), "cannot load libnccl.so.2: %s", dlerror());
+        return err;
+    }
+#define IBGM_SYM(field, name)                                             \
+    g_nccl.field = reinterpret_cast<decltype(g_nccl.field)>(dlsym(h, name)); \
+    if (!g_nccl.field) {                                                  \
+        snprintf(err, sizeof(err), "libnccl.so.2 lacks %s", name);        \
+        return err;                                                       \
+    }
+    IBGM_SYM(GetUniqueId, "ncclGetUniqueId");
+    IBGM_SYM(CommInitRank, "ncclCommInitRank");
+    IBGM_SYM(CommDestroy, "ncclCommDestroy");
+    IBGM_SYM(AllReduce, "ncclAllReduce");
+    IBGM_SYM(AllGather, "ncclAllGather");
+    IBGM_SYM(Send, "ncclSend");
+    IBGM_SYM(Recv, "ncclRecv");
+    IBGM_SYM(GroupStart, "ncclGroupStart");
+    IBGM_SYM(GroupEnd, "ncclGroupEnd");
+    IBGM_SYM(GetErrorString, "ncclGetErrorString");
+#undef IBGM_SYM
+    g_nccl.ok = true;
+    return nullptr;
+}
+
+int nccl_unique_id(NcclUid* id) { return g_nccl.GetUniqueId(id); }
+int nccl_comm_init(void** comm, int nranks, const NcclUid* id, int rank) { return g_nccl.CommInitRank(comm, nranks, *id, rank); }
+void nccl_comm_destroy(void* comm) { if (comm && g_nccl.ok) g_nccl.CommDestroy(comm); }
+const char* nccl_error_string(int rc) { return g_nccl.ok ? g_nccl.GetErrorString(rc) : "nccl not loaded"; }
+
+// ------------------------------------------------------------------------------------
+// Slab line solve: device coefficient block (built on the host in long double by
+// make_slab_coef): header, then inv[m], cp[m], g[m], h[m] of the interior block
+// B = tridiag(c, a, b) of m = nz-1 unknowns, then S^{-1} (P x P) and its column sums.
+// ------------------------------------------------------------------------------------
+struct SlabCf {
+    const double* p;
+    int m, P;
+    __device__ __forceinline__ double c() const { return p[SC_C]; }
+    __device__ __forceinline__ double b() const { return p[SC_B]; }
+    __device__ __forceinline__ const double* inv() const { return p + SC_HDR; }
+    __device__ __forceinline__ const double* cp() const { return p + SC_HDR + m; }
+    __device__ __forceinline__ const double* g() const { return p + SC_HDR + 2 * m; }
+    __device__ __forceinline__ const double* h() const { return p + SC_HDR + 3 * m; }
+    __device__ __forceinline__ const double* sinv() const { return p + SC_HDR + 4 * m; }
+    __device__ __forceinline__ const double* colsum() const { return p + SC_HDR + 4 * m + P * P; }
+};
+
+enum SlabSrc { SRC_FIELD = 0, SRC_DIV = 1 };
+enum SlabEpi { EPI_STORE = 0, EPI_ADD_UN = 1 };
+
+struct SlabArgs {
+    double* io[3];            // per component: the slab field (plane-0 pointer)
+    const double* un[3];      // u^n (EPI_ADD_UN; SRC_DIV)
+    const double* unew[3];    // u^{n+1} (SRC_DIV)
+    double* p;                // SRC_DIV: p -> q = p - chi mu D.(u^{n+1}+u^n)/2
+    double* gather;           // [P][kSlots][plane]
+    double neg_rho_dt, chimu_half, invh;
+    int n, nz, rank;
+    long long plane;          // N^{d-1}
+};
+
+// forward phase: interior Thomas solve of every line of this slab, in place (plane 0
+// keeps d_0), and the per-line scalars of the reduced system:
+//   A_s = d_{s,0} - b f*_{s,1},  fm_s = f*_{s,m},  (mean fix) D_s = sum d,  F_s = sum f*.
+template <int DIM, int SRC, int MF>
+__global__ void __launch_bounds__(128) k_slab_fwd(SlabCf C, SlabArgs A, int slot0)
+{
+    const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (q >= A.plane) return;
+    const int comp = blockIdx.y;
+    double* io = (comp == 0) ? A.io[0] : (comp == 1 ? A.io[1] : A.io[2]);
+    const long long PL = A.plane;
+    const int n = A.n;
+    long long off[3] = {1, n, PL};      // +e_x, +e_y, +e_last (periodic in x, y within the slab)
+    if (SRC == SRC_DIV) {
+        const int i = (int)(q % n);
+        if (i == n - 1) off[0] = -(long long)(n - 1);
+        if (DIM == 3) {
+            const int j = (int)(q / n);
+            if (j == n - 1) off[1] = -(long long)(n - 1) * n;
+        } else {
+            off[1] = PL;                 // 2D: the cut axis is y
+        }
+    }
+    auto src = [&](int kl) -> double {
+        const long long f = kl * PL + q;
+        if (SRC == SRC_FIELD) return io[f];
+        // Step 3e RHS r = -(rho/dt) D.u^{n+1} and the explicit part of Step 3f
+        // (PAPER.md:484-491, 668-683); the +e_last neighbour of plane nz-1 is the halo
+        double dn = 0.0, dol = 0.0;
+#pragma unroll
+        for (int c = 0; c < DIM; ++c) {
+            const long long o = (c == DIM - 1) ? PL : off[c];
+            dn += A.unew[c][f + o] - A.unew[c][f];
+            dol += A.un[c][f + o] - A.un[c][f];
+        }
+        dn *= A.invh;
+        dol *= A.invh;
+        A.p[f] = A.p[f] - A.chimu_half * (dn + dol);
+        const double r = A.neg_rho_dt * dn;
+        io[f] = r;
+        return r;
+    };
+    const double c = C.c(), b = C.b();
+    const double* inv = C.inv();
+    const double* cpv = C.cp();
+    const int m = C.m;
+    const double d0 = src(0);
+    double dsum = d0, prev = 0.0;
+    for (int i = 1; i <= m; ++i) {
+        const double d = src(i);
+        dsum += d;
+        prev = (d - c * prev) * inv[i - 1];
+        io[i * PL + q] = prev;
+    }
+    double x = prev, fsum = prev;
+    const double fm = prev;
+    for (int i = m - 1; i >= 1; --i) {
+        x = io[i * PL + q] - cpv[i - 1] * x;
+        io[i * PL + q] = x;
+        fsum += x;
+    }
+    double* g = A.gather + ((long long)A.rank * kSlabSlots + slot0 + 2 * comp) * PL;
+    g[q] = d0 - b * x;                  // x = f*_1 here
+    g[PL + q] = fm;
+    if (MF) {
+        g[2 * PL + q] = dsum;
+        g[3 * PL + q] = fsum;
+    }
+}
+
+// correction phase: r_t = A_t - c fm_{t-1} for every part t (all ranks' scalars are in
+// the gather buffer), y_s = (S^{-1} r)_s, y_{s+1}; x = f* - c y_s g - b y_{s+1} h; the
+// exact line-mean correction (R16) uses sum(y) = colsum(S^{-1}) . r and
+// sum(x) = (1 - c gsum - b hsum) sum(y) + sum_t F_t.
+template <int EPI, int MF>
+__global__ void __launch_bounds__(128) k_slab_corr(SlabCf C, SlabArgs A, int slot0)
+{
+    const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (q >= A.plane) return;
+    const int comp = blockIdx.y;
+    double* io = (comp == 0) ? A.io[0] : (comp == 1 ? A.io[1] : A.io[2]);
+    const double* un = (comp == 0) ? A.un[0] : (comp == 1 ? A.un[1] : A.un[2]);
+    const long long PL = A.plane;
+    const int P = C.P, s = A.rank, s1 = (A.rank + 1) % C.P;
+    slot0 += 2 * comp;                  // component c uses slots slot0 + 2c, slot0 + 2c + 1
+    const double c = C.c(), b = C.b();
+    const double* SI = C.sinv();
+    const double* CS = C.colsum();
+    double ys = 0.0, ys1 = 0.0, ysum = 0.0, D = 0.0, F = 0.0;
+    for (int t = 0; t < P; ++t) {
+        const int tp = (t == 0) ? P - 1 : t - 1;
+        const double* gt = A.gather + ((long long)t * kSlabSlots + slot0) * PL;
+        const double* gp = A.gather + ((long long)tp * kSlabSlots + slot0) * PL;
+        const double r = gt[q] - c * gp[PL + q];
+        ys = fma(SI[s * P + t], r, ys);
+        ys1 = fma(SI[s1 * P + t], r, ys1);
+        if (MF) {
+            ysum = fma(CS[t], r, ysum);
+            D += gt[2 * PL + q];
+            F += gt[3 * PL + q];
+        }
+    }
+    double corr = 0.0;
+    if (MF) {
+        const double X = (1.0 - c * C.p[SC_GSUM] - b * C.p[SC_HSUM]) * ysum + F;
+        corr = (D * C.p[SC_INVROW] - X) / C.p[SC_N];
+    }
+    const double* g = C.g();
+    const double* h = C.h();
+    const double cy = c * ys, by = b * ys1;
+    for (int kl = 0; kl <= C.m; ++kl) {
+        const long long f = kl * PL + q;
+        double x = (kl == 0) ? ys : io[f] - (cy * g[kl - 1] + by * h[kl - 1]);
+        x += corr;
+        if (EPI == EPI_ADD_UN) io[f] = un[f] + x;     // u^{n+1} = u^n + delta (R23)
+        else io[f] = x;
+    }
+}
+
+static unsigned nb128(long long cnt) { return (unsigned)((cnt + 127) / 128); }
+
+static SlabArgs slab_args(Ctx* s, Group* G)
+{
+    SlabArgs a{};
+    a.gather = G->gather;
+    a.n = (int)s->n;
+    a.nz = (int)s->nl;
+    a.rank = s->rank;
+    a.plane = s->plane;
+    a.invh = 1.0 / s->h;
+    a.neg_rho_dt = -s->rho / s->dt;
+    a.chimu_half = 0.5 * s->chi * s->mu;
+    return a;
+}
+
+// viscous sweep along the cut axis, all components: st = u^n + (1 - A_last)^{-1} st
+cudaError_t slab_sweep_last_fwd(Ctx* s, Group* G)
+{
+    SlabArgs a = slab_args(s, G);
+    for (int c = 0; c < s->dim; ++c) { a.io[c] = s->st[c]; a.un[c] = s->u[c]; }
+    SlabCf C{G->coef[SYS_VISC], (int)s->nl - 1, G->P};
+    dim3 grid(nb128(s->plane), (unsigned)s->dim);
+    if (s->dim == 3) k_slab_fwd<3, SRC_FIELD, 0><<<grid, 128, 0, s->stream>>>(C, a, 0);
+    else k_slab_fwd<2, SRC_FIELD, 0><<<grid, 128, 0, s->stream>>>(C, a, 0);
+    s->launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t slab_sweep_last_corr(Ctx* s, Group* G)
+{
+    SlabArgs a = slab_args(s, G);
+    for (int c = 0; c < s->dim; ++c) { a.io[c] = s->st[c]; a.un[c] = s->u[c]; }
+    SlabCf C{G->coef[SYS_VISC], (int)s->nl - 1, G->P};
+    k_slab_corr<EPI_ADD_UN, 0><<<dim3(nb128(s->plane), (unsigned)s->dim), 128, 0, s->stream>>>(C, a, 0);
+    s->launches++;
+    return cudaGetLastError();
+}
+
+// Step 3e RHS, explicit part of 3f and the psi factor along the cut axis (into p*)
+cudaError_t slab_divpsi_fwd(Ctx* s, Group* G)
+{
+    SlabArgs a = slab_args(s, G);
+    a.io[0] = a.io[1] = a.io[2] = s->pstar;
+    for (int c = 0; c < s->dim; ++c) { a.un[c] = s->u[c]; a.unew[c] = s->st[c]; }
+    a.p = s->p;
+    SlabCf C{G->coef[SYS_PSI], (int)s->nl - 1, G->P};
+    if (s->dim == 3) k_slab_fwd<3, SRC_DIV, 1><<<dim3(nb128(s->plane), 1), 128, 0, s->stream>>>(C, a, 0);
+    else k_slab_fwd<2, SRC_DIV, 1><<<dim3(nb128(s->plane), 1), 128, 0, s->stream>>>(C, a, 0);
+    s->launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t slab_divpsi_corr(Ctx* s, Group* G)
+{
+    SlabArgs a = slab_args(s, G);
+    a.io[0] = a.io[1] = a.io[2] = s->pstar;
+    SlabCf C{G->coef[SYS_PSI], (int)s->nl - 1, G->P};
+    k_slab_corr<EPI_STORE, 1><<<dim3(nb128(s->plane), 1), 128, 0, s->stream>>>(C, a, 0);
+    s->launches++;
+    return cudaGetLastError();
+}
+
+// stand-alone solve along the cut axis of data (in place) with coefficient block sys
+cudaError_t slab_user_fwd(Ctx* s, Group* G, double* data, int mf)
+{
+    SlabArgs a = slab_args(s, G);
+    a.io[0] = a.io[1] = a.io[2] = data;
+    SlabCf C{G->coef[SYS_USER], (int)s->nl - 1, G->P};
+    const dim3 grid(nb128(s->plane), 1);
+    if (mf) {
+        if (s->dim == 3) k_slab_fwd<3, SRC_FIELD, 1><<<grid, 128, 0, s->stream>>>(C, a, 0);
+        else k_slab_fwd<2, SRC_FIELD, 1><<<grid, 128, 0, s->stream>>>(C, a, 0);
+    } else {
+        if (s->dim == 3) k_slab_fwd<3, SRC_FIELD, 0><<<grid, 128, 0, s->stream>>>(C, a, 0);
+        else k_slab_fwd<2, SRC_FIELD, 0><<<grid, 128, 0, s->stream>>>(C, a, 0);
+    }
+    s->launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t slab_user_corr(Ctx* s, Group* G, double* data, int mf)
+{
+    SlabArgs a = slab_args(s, G);
+    a.io[0] = a.io[1] = a.io[2] = data;
+    SlabCf C{G->coef[SYS_USER], (int)s->nl - 1, G->P};
+    const dim3 grid(nb128(s->plane), 1);
+    if (mf) k_slab_corr<EPI_STORE, 1><<<grid, 128, 0, s->stream>>>(C, a, 0);
+    else k_slab_corr<EPI_STORE, 0><<<grid, 128, 0, s->stream>>>(C, a, 0);
+    s->launches++;
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------
+// IB on a slab
+// ------------------------------------------------------------------------------------
+template <int KER>
+__device__ __forceinline__ void w4(double x, int n, int& i0, double w[4])
+{
+    const double fl = floor(x);
+    const double r = x - fl;
+    long long b = (long long)fl - 1;
+    b %= n;
+    if (b < 0) b += n;
+    i0 = (int)b;
+    if (KER == IB_DELTA_COS4) {
+        double sn, cs;
+        sincospi(0.5 * r, &sn, &cs);
+        w[0] = 0.25 * (1.0 - sn);
+        w[1] = 0.25 * (1.0 + cs);
+        w[2] = 0.25 * (1.0 + sn);
+        w[3] = 0.25 * (1.0 - cs);
+    } else {
+        const double qq = sqrt(1.0 + 4.0 * r - 4.0 * r * r);
+        w[0] = 0.125 * (3.0 - 2.0 * r - qq);
+        w[1] = 0.125 * (3.0 - 2.0 * r + qq);
+        w[2] = 0.125 * (1.0 + 2.0 * r + qq);
+        w[3] = 0.125 * (1.0 + 2.0 * r - qq);
+    }
+}
+
+__device__ __forceinline__ int wrapp(int i, int n) { return i >= n ? i - n : i; }
+
+// Step 1a restricted to the nodes this slab owns (global planes z0 .. z0+nz-1 of the
+// last axis): Upart_k = sum over owned stencil nodes of u phi phi (phi).  The sum over
+// ranks (all-reduce) is U^n of PAPER.md:581-586.
+template <int DIM, int KER>
+__global__ void k_interp_part(const double* __restrict__ u0, const double* __restrict__ u1,
+                              const double* __restrict__ u2, const double* __restrict__ X,
+                              double* __restrict__ Upart, long long npts, int n, int z0, int nz, double invh)
+{
+    const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (k >= npts) return;
+    double Xk[3];
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) Xk[a] = X[k * DIM + a];
+    const long long nn = n;
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) {
+        const double* uc = (c == 0) ? u0 : (c == 1 ? u1 : u2);
+        int i0[3] = {0, 0, 0};
+        double w[3][4];
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) w4<KER>(Xk[a] * invh - (a == c ? 0.0 : 0.5), n, i0[a], w[a]);
+        double acc = 0.0;
+#pragma unroll
+        for (int mL = 0; mL < 4; ++mL) {
+            const int kl = wrapp(i0[DIM - 1] + mL, n) - z0;
+            if (kl < 0 || kl >= nz) continue;
+            double pa = 0.0;
+            if (DIM == 2) {
+                const long long row = nn * kl;
+#pragma unroll
+                for (int m0 = 0; m0 < 4; ++m0) pa += w[0][m0] * uc[row + wrapp(i0[0] + m0, n)];
+            } else {
+                const long long pl = nn * nn * kl;
+#pragma unroll
+                for (int m1 = 0; m1 < 4; ++m1) {
+                    const long long row = pl + nn * wrapp(i0[1] + m1, n);
+                    double r = 0.0;
+#pragma unroll
+                    for (int m0 = 0; m0 < 4; ++m0) r += w[0][m0] * uc[row + wrapp(i0[0] + m0, n)];
+                    pa += w[1][m1] * r;
+                }
+            }
+            acc += w[DIM - 1][mL] * pa;
+        }
+        Upart[k * DIM + c] = acc;
+    }
+}
+
+// sum of the P partial interpolations (EMULATE transport; NCCL all-reduces instead)
+__global__ void k_sum_slots(const double* __restrict__ part, int P, long long cnt, double* __restrict__ out)
+{
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < cnt; q += (long long)gridDim.x * blockDim.x) {
+        double a = 0.0;
+        for (int r = 0; r < P; ++r) a += part[r * cnt + q];
+        out[q] = a;
+    }
+}
+
+// Steps 1b-1c on every point from the reduced U^n (identical on every rank)
+__global__ void k_evolve(const double* __restrict__ U, double* __restrict__ X, double* __restrict__ Xh,
+                         double* __restrict__ Uprev, long long cnt, double dt, int first)
+{
+    const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (e >= cnt) return;
+    const double x = X[e], u = U[e];
+    const double xn = first ? x + dt * u : x + dt * (1.5 * u - 0.5 * Uprev[e]);
+    Xh[e] = 0.5 * (xn + x);
+    X[e] = xn;
+    Uprev[e] = u;
+}
+
+// Step 2b restricted to the nodes this slab owns (into G = N^{n-1} + (2/rho) f, R24)
+template <int DIM, int KER, bool KEEP>
+__global__ void __launch_bounds__(128) k_spread_part(const double* __restrict__ Xh, const double* __restrict__ F,
+                                                     const double* __restrict__ wgt, double* g0, double* g1, double* g2,
+                                                     double* f0, double* f1, double* f2, long long npts, int n, int z0,
+                                                     int nz, double invh, double invhd, double two_rho)
+{
+    const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (k >= npts) return;
+    double Xk[3];
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) Xk[a] = Xh[k * DIM + a];
+    const double wk = wgt[k] * invhd;
+    const long long nn = n;
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) {
+        double* gc = (c == 0) ? g0 : (c == 1 ? g1 : g2);
+        double* fc = (c == 0) ? f0 : (c == 1 ? f1 : f2);
+        int i0[3] = {0, 0, 0};
+        double w[3][4];
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) w4<KER>(Xk[a] * invh - (a == c ? 0.0 : 0.5), n, i0[a], w[a]);
+        const double Fc = F[k * DIM + c] * wk;
+#pragma unroll
+        for (int mL = 0; mL < 4; ++mL) {
+            const int kl = wrapp(i0[DIM - 1] + mL, n) - z0;
+            if (kl < 0 || kl >= nz) continue;
+            const double aL = Fc * w[DIM - 1][mL];
+            if (DIM == 2) {
+                const long long row = nn * kl;
+#pragma unroll
+                for (int m0 = 0; m0 < 4; ++m0) {
+                    const long long q = row + wrapp(i0[0] + m0, n);
+                    const double v = aL * w[0][m0];
+                    atomicAdd(gc + q, two_rho * v);
+                    if (KEEP) atomicAdd(fc + q, v);
+                }
+            } else {
+                const long long pl = nn * nn * kl;
+#pragma unroll
+                for (int m1 = 0; m1 < 4; ++m1) {
+                    const long long row = pl + nn * wrapp(i0[1] + m1, n);
+                    const double a1 = aL * w[1][m1];
+#pragma unroll
+                    for (int m0 = 0; m0 < 4; ++m0) {
+                        const long long q = row + wrapp(i0[0] + m0, n);
+                        const double v = a1 * w[0][m0];
+                        atomicAdd(gc + q, two_rho * v);
+                        if (KEEP) atomicAdd(fc + q, v);
+                    }
+                }
+            }
+        }
+    }
+}
+
+cudaError_t slab_interp_part(Ctx* top, Ctx* s, double* Upart)
+{
+    const double invh = 1.0 / s->h;
+#define IBGM_IP(D, K) k_interp_part<D, K><<<nb128(top->npts), 128, 0, s->stream>>>( \
+        s->u[0], s->u[1], s->u[2], top->X, Upart, top->npts, (int)s->n, (int)s->z0, (int)s->nl, invh)
+    if (s->dim == 2) { if (top->kernel == IB_DELTA_COS4) IBGM_IP(2, 0); else IBGM_IP(2, 1); }
+    else { if (top->kernel == IB_DELTA_COS4) IBGM_IP(3, 0); else IBGM_IP(3, 1); }
+#undef IBGM_IP
+    s->launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t slab_sum_slots(Ctx* top, const double* part, int P, double* out)
+{
+    const long long cnt = top->npts * top->dim;
+    k_sum_slots<<<(unsigned)((cnt + 255) / 256 < 592 ? (cnt + 255) / 256 : 592), 256, 0, top->stream>>>(part, P, cnt, out);
+    top->launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t slab_evolve(Ctx* top, const double* U, int first)
+{
+    const long long cnt = top->npts * top->dim;
+    k_evolve<<<nb128(cnt), 128, 0, top->stream>>>(U, top->X, top->Xh, top->Uprev, cnt, top->dt, first);
+    top->launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t slab_spread_part(Ctx* top, Ctx* s)
+{
+    const double invh = 1.0 / s->h;
+    const double invhd = (s->dim == 3) ? invh * invh * invh : invh * invh;
+    const bool kp = top->debug_keep_f != 0;
+#define IBGM_SPP(D, K, KP) k_spread_part<D, K, KP><<<nb128(top->npts), 128, 0, s->stream>>>(                       \
+        top->Xh, top->F, top->wgt, s->nprev[0], s->nprev[1], s->nprev[2], s->f[0], s->f[1], s->f[2], top->npts, \
+        (int)s->n, (int)s->z0, (int)s->nl, invh, invhd, 2.0 / s->rho)
+    if (s->dim == 2) {
+        if (top->kernel == IB_DELTA_COS4) { if (kp) IBGM_SPP(2, 0, true); else IBGM_SPP(2, 0, false); }
+        else { if (kp) IBGM_SPP(2, 1, true); else IBGM_SPP(2, 1, false); }
+    } else {
+        if (top->kernel == IB_DELTA_COS4) { if (kp) IBGM_SPP(3, 0, true); else IBGM_SPP(3, 0, false); }
+        else { if (kp) IBGM_SPP(3, 1, true); else IBGM_SPP(3, 1, false); }
+    }
+#undef IBGM_SPP
+    s->launches++;
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------
+// transports
+// ------------------------------------------------------------------------------------
+#define NCK(call)                                   \
+    do {                                            \
+        const int r_ = (call);                      \
+        if (r_ != 0) return r_;                     \
+    } while (0)
+
+// Halo exchange of the listed fields.  dir_up: plane nz-1 of slab s
+// -> plane -1 of slab s+1; dir_down: plane 0 of slab s -> plane nz of slab s-1 (periodic).
+// Returns 0, a cudaError_t (as int, transport EMULATE) or an ncclResult_t (NCCL).
+int group_halo(Group* G, int nf, const HaloSpec* spec, cudaStream_t st)
+{
+    const int P = G->P;
+    if (G->transport == IB_TRANSPORT_EMULATE) {
+        for (int f = 0; f < nf; ++f)
+            for (int r = 0; r < P; ++r) {
+                Ctx* a = G->slab[r];
+                const size_t pb = (size_t)a->plane * sizeof(double);
+                const long long nz = a->nl, PL = a->plane;
+                if (spec[f].up) {
+                    Ctx* b = G->slab[(r + 1) % P];
+                    cudaError_t e = cudaMemcpyAsync(spec[f].field(b) - PL, spec[f].field(a) + (nz - 1) * PL, pb,
+                                                    cudaMemcpyDeviceToDevice, st);
+                    if (e != cudaSuccess) return (int)e;
+                }
+                if (spec[f].down) {
+                    Ctx* b = G->slab[(r + P - 1) % P];
+                    cudaError_t e = cudaMemcpyAsync(spec[f].field(b) + nz * PL, spec[f].field(a), pb,
+                                                    cudaMemcpyDeviceToDevice, st);
+                    if (e != cudaSuccess) return (int)e;
+                }
+            }
+        return 0;
+    }
+    Ctx* a = G->slab[0];
+    const long long nz = a->nl, PL = a->plane;
+    const int up = (G->rank + 1) % P, dn = (G->rank + P - 1) % P;
+    NCK(g_nccl.GroupStart());
+    for (int f = 0; f < nf; ++f) {
+        double* fld = spec[f].field(a);
+        if (spec[f].up) {
+            NCK(g_nccl.Send(fld + (nz - 1) * PL, (size_t)PL, kNcclDouble, up, G->comm, st));
+            NCK(g_nccl.Recv(fld - PL, (size_t)PL, kNcclDouble, dn, G->comm, st));
+        }
+        if (spec[f].down) {
+            NCK(g_nccl.Send(fld, (size_t)PL, kNcclDouble, dn, G->comm, st));
+            NCK(g_nccl.Recv(fld + nz * PL, (size_t)PL, kNcclDouble, up, G->comm, st));
+        }
+    }
+    NCK(g_nccl.GroupEnd());
+    return 0;
+}
+
+// every rank's reduced-system scalars to every rank (EMULATE: the buffer is shared)
+int group_allgather(Group* G, cudaStream_t st)
+{
+    if (G->transport == IB_TRANSPORT_EMULATE) return 0;
+    const size_t cnt = (size_t)kSlabSlots * G->slab[0]->plane;
+    return g_nccl.AllGather(G->gather + (size_t)G->rank * cnt, G->gather, cnt, kNcclDouble, G->comm, st);
+}
+
+// U^n = sum over ranks of the partial interpolations
+int group_allreduce_U(Group* G, Ctx* top, cudaStream_t st)
+{
+    const long long cnt = top->npts * top->dim;
+    if (G->transport == IB_TRANSPORT_EMULATE) return (int)slab_sum_slots(top, G->Upart, G->P, G->Ured);
+    return g_nccl.AllReduce(G->Upart, G->Ured, (size_t)cnt, kNcclDouble, kNcclSum, G->comm, st);
+}
+
+}  // namespace ibgm

@@ -15,6 +15,8 @@ from . import _build
 
 IB_DELTA_COS4 = 0
 IB_DELTA_PESKIN4 = 1
+IB_TRANSPORT_NCCL = 0
+IB_TRANSPORT_EMULATE = 1
 
 _dp = ctypes.POINTER(ctypes.c_double)
 _i64p = ctypes.POINTER(ctypes.c_int64)
@@ -33,14 +35,14 @@ class ib_grid(ctypes.Structure):
 class ib_options(ctypes.Structure):
     _fields_ = [("kernel", ctypes.c_int32), ("chi", ctypes.c_double), ("advection", ctypes.c_int32),
                 ("device", ctypes.c_int32), ("stream", ctypes.c_void_p), ("rank", ctypes.c_int32),
-                ("nranks", ctypes.c_int32)]
+                ("nranks", ctypes.c_int32), ("transport", ctypes.c_int32), ("nccl_id", ctypes.c_void_p)]
 
 
 _lib = None
 SYMBOLS = ["ib_default_options", "ib_create", "ib_set_fields", "ib_set_boundary", "ib_set_fibers",
            "ib_step", "ib_sync", "ib_get_fields", "ib_get_aux", "ib_line_solve", "ib_check_finite",
            "ib_get_stats", "ib_destroy", "ib_last_error", "ib_set_profiling", "ib_get_phase_times",
-           "ib_set_debug"]
+           "ib_set_debug", "ib_nccl_unique_id", "ib_slab_range"]
 
 PHASES = ["interp_evolve", "force", "spread", "s1_rhs_xsweep", "sweep_y", "sweep_z", "div_psi_first",
           "psi_y", "psi_x_p", "clear"]
@@ -80,6 +82,8 @@ def lib():
         L.ib_set_profiling.argtypes = [ctypes.c_void_p, ctypes.c_int32]
         L.ib_get_phase_times.argtypes = [ctypes.c_void_p, _dp, _i64p]
         L.ib_set_debug.argtypes = [ctypes.c_void_p, ctypes.c_int32]
+        L.ib_nccl_unique_id.argtypes = [ctypes.c_void_p]
+        L.ib_slab_range.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, _i64p, _i64p]
         for name in SYMBOLS:
             if name not in ("ib_default_options", "ib_last_error"):
                 getattr(L, name).restype = ctypes.c_int
@@ -104,18 +108,53 @@ def _c(a):
     return None if a is None else np.ascontiguousarray(a, dtype=np.float64)
 
 
+def nccl_unique_id() -> bytes:
+    """ib_nccl_unique_id: 128 bytes for rank 0 to share with every rank."""
+    buf = ctypes.create_string_buffer(128)
+    _ck(lib().ib_nccl_unique_id(buf))
+    return buf.raw
+
+
+def slab_range(n, nranks, rank):
+    """ib_slab_range: (z0, nz) of rank's slab along the cut axis."""
+    z0, nz = ctypes.c_int64(), ctypes.c_int64()
+    _ck(lib().ib_slab_range(n, nranks, rank, ctypes.byref(z0), ctypes.byref(nz)))
+    return z0.value, nz.value
+
+
+def share_nccl_id(group=None) -> bytes:
+    """Rank 0 creates the NCCL unique id; torch.distributed broadcasts it (any backend)."""
+    import torch.distributed as dist
+    obj = [nccl_unique_id() if dist.get_rank() == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    return obj[0]
+
+
 class Context:
-    """One IB-GM problem on one GPU: ib_create(grid, nu, rho, dt)."""
+    """One IB-GM problem: ib_create(grid, nu, rho, dt).
+
+    nranks > 1 cuts the grid into z-slabs: transport
+    IB_TRANSPORT_NCCL holds this rank's slab (fields are local, nccl_id from
+    share_nccl_id()), IB_TRANSPORT_EMULATE holds all slabs on one GPU (fields are
+    global)."""
 
     def __init__(self, dim, n, nu, rho, dt, *, kernel=IB_DELTA_COS4, chi=0.6, advection=True, device=0,
-                 stream=None):
+                 stream=None, nranks=1, rank=0, transport=IB_TRANSPORT_NCCL, nccl_id=None):
         L = lib()
         self.dim, self.n = dim, n
+        self.nranks, self.rank, self.transport = nranks, rank, transport
+        self.local = nranks > 1 and transport == IB_TRANSPORT_NCCL
+        self.nz = n // nranks if self.local else n
         g = ib_grid(dim, n, 1.0)
         o = ib_options()
         L.ib_default_options(ctypes.byref(o))
         o.kernel, o.chi, o.advection, o.device = kernel, chi, int(advection), device
         o.stream = stream
+        o.nranks, o.rank, o.transport = nranks, rank, transport
+        self._id = None
+        if nccl_id is not None:
+            self._id = ctypes.create_string_buffer(bytes(nccl_id), 128)
+            o.nccl_id = ctypes.cast(self._id, ctypes.c_void_p)
         h = ctypes.c_void_p()
         rc = L.ib_create(ctypes.byref(g), nu, rho, dt, ctypes.byref(o), ctypes.byref(h))
         self._h = h
@@ -129,7 +168,9 @@ class Context:
 
     @property
     def shape(self):
-        return (self.n,) * self.dim
+        """Shape of the field arrays this context takes and returns (the local slab with
+        the NCCL transport)."""
+        return (self.nz,) + (self.n,) * (self.dim - 1)
 
     def close(self):
         if getattr(self, "_h", None):
@@ -219,10 +260,21 @@ class Context:
         return dict(kernel_launches=a.value, steps=b.value)
 
 
+def slab_of(a, nranks, rank):
+    """The planes of rank's slab of a global field (cut along the first array axis =
+    the last grid axis)."""
+    nz = a.shape[0] // nranks
+    return np.ascontiguousarray(a[rank * nz:(rank + 1) * nz])
+
+
 def from_problem(pr, **kw):
-    """Context + state from an inputs.Problem."""
+    """Context + state from an inputs.Problem (fields cut to the local slab when the
+    context holds one)."""
     ctx = Context(pr.dim, pr.n, pr.mu / pr.rho, pr.rho, pr.dt, kernel=pr.kernel, chi=pr.chi, **kw)
-    ctx.set_fields(*pr.u, p=pr.p) if pr.dim == 3 else ctx.set_fields(pr.u[0], pr.u[1], None, pr.p)
+    cut = (lambda a: a if a is None or not ctx.local else slab_of(a, ctx.nranks, ctx.rank))
+    u = [cut(x) for x in pr.u]
+    p = cut(pr.p)
+    ctx.set_fields(*u, p=p) if pr.dim == 3 else ctx.set_fields(u[0], u[1], None, p)
     if pr.X is not None:
         ctx.set_boundary(pr.X, pr.edges, pr.kappa, rest=pr.rest, weight=pr.weight)
     return ctx
