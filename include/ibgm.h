@@ -80,7 +80,9 @@ typedef struct {
     void* stream;      /* cudaStream_t to order all work on, or NULL (own stream)       */
     int32_t rank;      /* z-slab rank in [0, nranks) (NCCL transport; 0 otherwise)     */
     int32_t nranks;    /* number of z-slabs, default 1 (no decomposition); N % nranks
-                          == 0 and N/nranks >= 2                                        */
+                          == 0 and N/nranks >= 2.  nranks = 1 with transport EMULATE or
+                          with an nccl_id runs the slab code path on one slab (a 1-rank
+                          communicator for NCCL: tests the transport on one GPU)        */
     int32_t transport; /* IB_TRANSPORT_NCCL (default) | IB_TRANSPORT_EMULATE            */
     const void* nccl_id; /* NCCL transport, nranks > 1: the 128-byte unique id that rank 0
                           obtained from ib_nccl_unique_id and shared with every rank
@@ -179,9 +181,16 @@ int ib_get_stats(ib_ctx* ctx, int64_t* kernel_launches, int64_t* steps_done);
 
 /* Debug flags: bit 0 keeps the spread force f^{n+1/2} as a separate field so that
  * ib_get_aux can return it (costs one extra atomic per spread contribution and a
- * clear per step).  Bits 1-2 select the spreading method: 0 automatic (per-point
- * atomics below 3e5 points, brick-binned above), 1 per-point atomics, 2 brick-binned.
- * Off / automatic by default. */
+ * clear per step).  Bits 1-3 select the spreading method: 0 automatic (= 4),
+ * 1 one thread per point (4^d global fp64 reductions per component), 2 brick-binned
+ * (points counting-sorted into 4^3-cell bricks every step, shared-memory tiles),
+ * 3 box-staged (chunks of 64 consecutive points accumulate in a shared-memory box,
+ * one global reduction per box node), 4 quad-lane (4 lanes per point and component,
+ * one per x-node of a stencil row, so each warp reduction is coalesced).  Bits 4-5
+ * select the interpolation: 0 automatic (= 1), 1 one thread per point, 2 box-staged,
+ * 3 quad-lane.  The points are kept internally in Morton order of their initial
+ * cells (outputs are returned in the caller's order).  Automatic by default.  Only
+ * the single-GPU path honours bits 1-5. */
 int ib_set_debug(ib_ctx* ctx, int32_t flags);
 
 /* Turn per-phase CUDA-event timing on (1) or off (0).  While on, ib_step records an

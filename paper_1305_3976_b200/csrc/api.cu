@@ -2,6 +2,7 @@
 // the line-solver factors, the per-step schedule, host<->device copies.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -152,6 +153,9 @@ void make_line_coef(LineCoef* C, SchurInv* SI, int64_t N, int L, double c_, doub
     C->gsum = (double)F.gsum;
     C->hsum = (double)F.hsum;
     for (int i = 0; i < F.P * F.P; ++i) SI->sinv[i] = (double)F.sinv[i];
+    for (int p = 0; p < F.P; ++p)
+        for (int q = 0; q < F.P; ++q) SI->sinvT[q * F.P + p] = SI->sinv[p * F.P + q];
+    C->inv_n = (double)(1.0L / (long double)N);
     for (int q = 0; q < F.P; ++q) SI->colsum[q] = (double)F.colsum[q];
 }
 
@@ -208,6 +212,9 @@ static void free_lagrangian(Ctx* s)
     cudaFree(s->X); cudaFree(s->Xh); cudaFree(s->Uprev); cudaFree(s->F); cudaFree(s->wgt);
     cudaFree(s->csr_ptr); cudaFree(s->csr_nbr); cudaFree(s->csr_kappa); cudaFree(s->csr_rest);
     cudaFree(s->bin_bid); cudaFree(s->bin_sorted);
+    cudaFree(s->pt_user); cudaFree(s->lag_tmp);
+    s->pt_user = nullptr;
+    s->lag_tmp = nullptr;
     s->bin_bid = s->bin_sorted = nullptr;
     s->X = s->Xh = s->Uprev = s->F = s->wgt = nullptr;
     s->csr_ptr = s->csr_nbr = nullptr;
@@ -296,6 +303,16 @@ static int upload_coef(Ctx* s, int sys, double c, double a, double b, int mf)
     return IB_OK;
 }
 
+// a Lagrangian array [npts][dim] to a host buffer in the caller's point order
+static cudaError_t points_out(Ctx* s, const double* dev, double* host)
+{
+    if (!host || s->npts == 0) return cudaSuccess;
+    cudaError_t e = launch_scatter_pts(s, dev, s->lag_tmp);
+    if (e != cudaSuccess) return e;
+    return cudaMemcpyAsync(host, s->lag_tmp, (size_t)s->npts * s->dim * sizeof(double), cudaMemcpyDeviceToHost,
+                           s->stream);
+}
+
 extern "C" {
 
 void ib_default_options(ib_options* o)
@@ -353,7 +370,10 @@ int ib_create(const ib_grid* grid, double nu, double rho, double dt, const ib_op
         return fail(IB_EINVAL, "unknown transport %d", o.transport);
     const int P = o.nranks;
     if (P < 1) return fail(IB_EINVAL, "nranks must be >= 1");
-    if (P > 1) {
+    // the slab path also runs with one slab when asked for explicitly (EMULATE, or an
+    // NCCL id: a 1-rank communicator), which exercises the transports on one GPU
+    const bool slab = P > 1 || o.transport == IB_TRANSPORT_EMULATE || o.nccl_id != nullptr;
+    if (slab) {
         const int rc = ib_slab_range(grid->n, P, o.transport == IB_TRANSPORT_NCCL ? o.rank : 0, nullptr, nullptr);
         if (rc != IB_OK) return rc;
         if (o.transport == IB_TRANSPORT_EMULATE && o.rank != 0) return fail(IB_EINVAL, "EMULATE transport: rank must be 0");
@@ -407,7 +427,7 @@ int ib_create(const ib_grid* grid, double nu, double rho, double dt, const ib_op
     make_line_coef(&s->hcoef[SYS_USER], &hs[SYS_USER], s->n, L, -kv, 1.0 + 2.0 * kv, -kv, 0);
     CKC(cudaMemcpyAsync(s->sinv, hs, sizeof(SchurInv) * SYS_COUNT, cudaMemcpyHostToDevice, s->stream));
 
-    if (P == 1) {
+    if (!slab) {
         s->nlocal = s->ncell;
         s->hoff = 0;
         CKC(alloc_fields(s));
@@ -521,15 +541,38 @@ int ib_set_boundary(ib_ctx* c, int64_t npts, const double* X, int64_t nedges, co
     s->step = 0;
     if (npts == 0) return IB_OK;
     const int d = s->dim;
-    // CSR adjacency: every edge appears in the lists of both endpoints
+    // internal order: Morton order of the cells holding the initial positions, so that
+    // consecutive points (one CTA of the box-staged interpolation / spreading) are close
+    // in space; ord[i] = caller index of internal point i, inv = its inverse
+    std::vector<int32_t> ord(npts), inv(npts);
+    {
+        std::vector<uint64_t> key(npts);
+        for (int64_t k = 0; k < npts; ++k) {
+            uint64_t code = 0;
+            for (int a = 0; a < d; ++a) {
+                long long ci = (long long)floor(X[k * d + a] / s->h);
+                ci %= s->n;
+                if (ci < 0) ci += s->n;
+                for (int bit = 0; bit < 11; ++bit) code |= (uint64_t)((ci >> bit) & 1) << (bit * d + a);
+            }
+            key[k] = code;
+        }
+        for (int64_t k = 0; k < npts; ++k) ord[k] = (int32_t)k;
+        std::stable_sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) { return key[a] < key[b]; });
+        for (int64_t i = 0; i < npts; ++i) inv[ord[i]] = (int32_t)i;
+    }
+    std::vector<double> Xi((size_t)npts * d);
+    for (int64_t i = 0; i < npts; ++i)
+        for (int a = 0; a < d; ++a) Xi[i * d + a] = X[(int64_t)ord[i] * d + a];
+    // CSR adjacency in internal indices: every edge appears in the lists of both endpoints
     std::vector<int32_t> ptr(npts + 1, 0), nbr(2 * nedges);
     std::vector<double> kap(2 * nedges), rst(2 * nedges);
-    for (int64_t e = 0; e < nedges; ++e) { ptr[edges[2 * e] + 1]++; ptr[edges[2 * e + 1] + 1]++; }
+    for (int64_t e = 0; e < nedges; ++e) { ptr[inv[edges[2 * e]] + 1]++; ptr[inv[edges[2 * e + 1]] + 1]++; }
     for (int64_t k = 0; k < npts; ++k) ptr[k + 1] += ptr[k];
     std::vector<int32_t> fill(ptr.begin(), ptr.end() - 1);
     int has_rest = 0;
     for (int64_t e = 0; e < nedges; ++e) {
-        const int64_t a = edges[2 * e], b = edges[2 * e + 1];
+        const int64_t a = inv[edges[2 * e]], b = inv[edges[2 * e + 1]];
         const double L = rest ? rest[e] : 0.0;
         if (L != 0.0) has_rest = 1;
         int32_t ia = fill[a]++, ib = fill[b]++;
@@ -537,7 +580,7 @@ int ib_set_boundary(ib_ctx* c, int64_t npts, const double* X, int64_t nedges, co
         nbr[ib] = (int32_t)a; kap[ib] = kappa[e]; rst[ib] = L;
     }
     std::vector<double> wv(npts, 1.0);
-    if (weight) for (int64_t k = 0; k < npts; ++k) wv[k] = weight[k];
+    if (weight) for (int64_t k = 0; k < npts; ++k) wv[k] = weight[ord[k]];
     const size_t pb = (size_t)npts * d * sizeof(double);
     CKC(cudaMalloc(&s->X, pb));
     CKC(cudaMalloc(&s->Xh, pb));
@@ -551,8 +594,11 @@ int ib_set_boundary(ib_ctx* c, int64_t npts, const double* X, int64_t nedges, co
     CKC(cudaMalloc(&s->csr_nbr, ne2 * sizeof(int32_t)));
     CKC(cudaMalloc(&s->csr_kappa, ne2 * sizeof(double)));
     CKC(cudaMalloc(&s->csr_rest, ne2 * sizeof(double)));
-    CKC(cudaMemcpyAsync(s->X, X, pb, cudaMemcpyHostToDevice, s->stream));
-    CKC(cudaMemcpyAsync(s->Xh, X, pb, cudaMemcpyHostToDevice, s->stream));
+    CKC(cudaMalloc(&s->pt_user, npts * sizeof(int32_t)));
+    CKC(cudaMalloc(&s->lag_tmp, pb));
+    CKC(cudaMemcpyAsync(s->pt_user, ord.data(), npts * sizeof(int32_t), cudaMemcpyHostToDevice, s->stream));
+    CKC(cudaMemcpyAsync(s->X, Xi.data(), pb, cudaMemcpyHostToDevice, s->stream));
+    CKC(cudaMemcpyAsync(s->Xh, Xi.data(), pb, cudaMemcpyHostToDevice, s->stream));
     CKC(cudaMemsetAsync(s->Uprev, 0, pb, s->stream));
     CKC(cudaMemsetAsync(s->F, 0, pb, s->stream));
     CKC(cudaMemcpyAsync(s->wgt, wv.data(), npts * sizeof(double), cudaMemcpyHostToDevice, s->stream));
@@ -854,7 +900,8 @@ int ib_set_debug(ib_ctx* c, int32_t flags)
     }
     drop_graphs(s);
     s->debug_keep_f = keep;
-    s->spread_mode = (flags >> 1) & 3;   // bits 1-2: spread method (0 auto, 1 direct, 2 brick)
+    s->spread_mode = (flags >> 1) & 7;   // bits 1-3: spreading method (include/ibgm.h)
+    s->interp_mode = (flags >> 4) & 3;   // bits 4-5: interpolation method
     return IB_OK;
 }
 
@@ -907,9 +954,8 @@ int ib_get_fields(ib_ctx* c, double* u, double* v, double* w, double* p, double*
             CKC(cudaMemcpyAsync(psi + off, sl->tmp, fb, cudaMemcpyDeviceToHost, s->stream));
         }
     }
-    const size_t pb = (size_t)s->npts * s->dim * sizeof(double);
-    if (X && pb) CKC(cudaMemcpyAsync(X, s->X, pb, cudaMemcpyDeviceToHost, s->stream));
-    if (U && pb) CKC(cudaMemcpyAsync(U, s->Uprev, pb, cudaMemcpyDeviceToHost, s->stream));
+    CKC(points_out(s, s->X, X));
+    CKC(points_out(s, s->Uprev, U));
     CKC(cudaStreamSynchronize(s->stream));
     return IB_OK;
 }
@@ -931,9 +977,8 @@ int ib_get_aux(ib_ctx* c, double* fu, double* fv, double* fw, double* nu, double
             if (no[q]) CKC(cudaMemcpyAsync(no[q] + off, sl->nprev[q], fb, cudaMemcpyDeviceToHost, s->stream));
         }
     }
-    const size_t pb = (size_t)s->npts * s->dim * sizeof(double);
-    if (F && pb) CKC(cudaMemcpyAsync(F, s->F, pb, cudaMemcpyDeviceToHost, s->stream));
-    if (Xh && pb) CKC(cudaMemcpyAsync(Xh, s->Xh, pb, cudaMemcpyDeviceToHost, s->stream));
+    CKC(points_out(s, s->F, F));
+    CKC(points_out(s, s->Xh, Xh));
     CKC(cudaStreamSynchronize(s->stream));
     return IB_OK;
 }

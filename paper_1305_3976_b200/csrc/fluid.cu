@@ -30,6 +30,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 
 #include "ibgm_internal.cuh"
 
@@ -133,7 +134,7 @@ __device__ __forceinline__ void ws_solve(double (&x)[L], const LineCoef& C, int 
         for (int i = 0; i < L; ++i) xs += x[i];
         const double D = group_sum<0>(dsum, P, gbase);
         const double X = group_sum<0>(xs, P, gbase);
-        const double corr = (D * C.inv_rowsum - X) / (double)(P * L);
+        const double corr = (D * C.inv_rowsum - X) * C.inv_n;
 #pragma unroll
         for (int i = 0; i < L; ++i) x[i] += corr;
     }
@@ -283,13 +284,13 @@ struct LArgs {
     int wrap;               // 1: the last axis is periodic here; 0: z-slab with halo planes
 };
 
-// Visit every (line l, position m) of the block's tile with coalesced global offsets:
-// consecutive threads take consecutive x.  f(l, m, q) with q the 32-bit flat index.
+// Visit every (line l, position m) of a tile with coalesced global offsets: consecutive
+// threads take consecutive x.  t / T: this thread's index among the T threads that
+// share the work.  f(l, m, q) with q the 32-bit flat index.
 // nrow bounds the rows of an x-line tile (the local planes of the last axis in 2D).
 template <int AX, class F>
-__device__ __forceinline__ void for_tile(int n, int nrow, int R, int g0, unsigned tb, F&& f)
+__device__ __forceinline__ void for_tile(int n, int nrow, int R, int g0, unsigned tb, int t, int T, F&& f)
 {
-    const int t = threadIdx.x, T = blockDim.x;
     const unsigned N = (unsigned)n;
     if (AX == 0) {
         if (n >= T) {
@@ -299,7 +300,7 @@ __device__ __forceinline__ void for_tile(int n, int nrow, int R, int g0, unsigne
                 for (int m = t; m < n; m += T) f(l, m, rb + (unsigned)m);
             }
         } else {
-            const int rows = T / n;          // rows covered per sweep of the block
+            const int rows = T / n;          // rows covered per sweep of the threads
             const int l0 = t / n, m = t - l0 * n;
             if (l0 >= rows) return;
             for (int l = l0; l < R && g0 + l < nrow; l += rows) f(l, m, (unsigned)m + N * (unsigned)(g0 + l) + N * N * tb);
@@ -315,91 +316,82 @@ __device__ __forceinline__ void for_tile(int n, int nrow, int R, int g0, unsigne
     }
 }
 
-template <int L, int KIND, int DIM, int AX, int NC, int MINB>
-__global__ void __launch_bounds__(256, MINB) k_lines(const LineCoef C, const SchurInv* __restrict__ SI, int n, int R,
-                                                     LArgs A)
-{
-    extern __shared__ double smem[];
-    const int P = C.P;
-    const int TP = tile_pitch(P, L);
-    double* sinvT = smem;
-    double* tile = smem + P * P;
-    double* tile2 = tile + (size_t)NC * R * TP;   // LAST: u^n, PSI_LAST: q (prefetched with the fill)
-    const int t = threadIdx.x, T = blockDim.x;
-    for (int e = t; e < P * P; e += T) {
-        const int q = e / P, sg = e - q * P;
-        sinvT[q * P + sg] = SI->sinv[sg * P + q];
-    }
-    const unsigned N = (unsigned)n;
-    const int comp = (NC == 1) ? blockIdx.z : 0;
-    const int g0 = blockIdx.x * R;              // first j (AX = 0) or first i (AX = 1, 2)
-    const unsigned tb = blockIdx.y;             // k (AX = 0, 1 in 3D) or j (AX = 2)
-    const unsigned RTP = (unsigned)R * TP;
-    const int nrow = (DIM == 2) ? A.nl : n;     // x-line rows (AX = 0)
-
-    // ---------------- fill (coalesced: consecutive threads -> consecutive x)
-    if (KIND == K_S1) {
-        if (n >= T) {
-            for (int l = 0; l < R && g0 + l < nrow; ++l) {
-                const RowB rb = row_bases<DIM>(g0 + l, (int)tb, n, A.nl, A.wrap);
-                for (int m = t; m < n; m += T) {
-                    double v[3];
-                    s1_cell<DIM>(A.s1, m, rb, n, v);
-                    const int off = tile_off<L>(l, m, TP);
-#pragma unroll
-                    for (int c = 0; c < NC; ++c) tile[c * RTP + off] = v[c];
-                }
-            }
-        } else {
-            const int rows = T / n;
-            const int l0 = t / n, m = t - l0 * n;
-            if (l0 < rows)
-                for (int l = l0; l < R && g0 + l < nrow; l += rows) {
-                    const RowB rb = row_bases<DIM>(g0 + l, (int)tb, n, A.nl, A.wrap);
-                    double v[3];
-                    s1_cell<DIM>(A.s1, m, rb, n, v);
-                    const int off = tile_off<L>(l, m, TP);
-#pragma unroll
-                    for (int c = 0; c < NC; ++c) tile[c * RTP + off] = v[c];
-                }
-        }
-    } else if (KIND == K_DIVPSI) {
-        // D.u at each cell for u^{n+1} and u^n
-        const unsigned stp[3] = {1u, N, N * N};
-        for_tile<AX>(n, nrow, R, g0, tb, [&](int l, int m, unsigned q) {
-            // cell coordinates along each axis: i = g0 + l; the line axis coordinate is m
-            int ijk[3];
-            ijk[0] = g0 + l;
-            if (AX == 1) { ijk[1] = m; ijk[2] = (int)tb; } else { ijk[1] = (int)tb; ijk[2] = m; }
-            double dn = 0.0, dol = 0.0;
-#pragma unroll
-            for (int c = 0; c < DIM; ++c) {
-                const unsigned qp = (ijk[c] == n - 1) ? q - (N - 1) * stp[c] : q + stp[c];
-                dn += ldg(A.unew[c] + qp) - ldg(A.unew[c] + q);
-                dol += ldg(A.un[c] + qp) - ldg(A.un[c] + q);
-            }
-            dn *= A.invh;
-            dol *= A.invh;
-            tile[tile_off<L>(l, m, TP)] = A.neg_rho_dt * dn;         // Step 3e RHS
-            A.p[q] = A.p[q] - A.chimu_half * (dn + dol);             // Step 3f, explicit part
-        });
-    } else {
-        // pure copies: cp.async keeps every load of the tile in flight at once
-        const double* src = (KIND == K_PSI_LAST) ? A.pstar : pick3<double*>(A.io[0], A.io[1], A.io[2], comp);
-        const double* src2 = (KIND == K_LAST) ? pick3<const double*>(A.un[0], A.un[1], A.un[2], comp)
-                                              : (KIND == K_PSI_LAST ? A.p : nullptr);
-        for_tile<AX>(n, nrow, R, g0, tb, [&](int l, int m, unsigned q) {
-            const int off = tile_off<L>(l, m, TP);
-            cp_async8(tile + off, src + q);
-            if (KIND == K_LAST || KIND == K_PSI_LAST) cp_async8(tile2 + off, src2 + q);
-        });
-        cp_async_wait_all();
-    }
-    __syncthreads();
-
-    // ---------------- solve: warp-synchronous, P lanes per line
+template <int L, int KIND, int DIM, int AX, int NC>
+struct LinePass {
+    // fill a tile (and tile2) for lines g0 .. g0+R-1 of slice tb (component comp)
+    static __device__ __forceinline__ void fill(double* tile, double* tile2, const LArgs& A, int n, int R, int TP,
+                                                int g0, unsigned tb, int comp, int t, int T)
     {
-        const int lane = t & 31, w = t >> 5, nw = T >> 5;
+        const unsigned N = (unsigned)n;
+        const unsigned RTP = (unsigned)R * TP;
+        const int nrow = (DIM == 2) ? A.nl : n;
+        if (KIND == K_S1) {
+            if (n >= T) {
+                for (int l = 0; l < R && g0 + l < nrow; ++l) {
+                    const RowB rb = row_bases<DIM>(g0 + l, (int)tb, n, A.nl, A.wrap);
+                    for (int m = t; m < n; m += T) {
+                        double v[3];
+                        s1_cell<DIM>(A.s1, m, rb, n, v);
+                        const int off = tile_off<L>(l, m, TP);
+#pragma unroll
+                        for (int c = 0; c < NC; ++c) tile[c * RTP + off] = v[c];
+                    }
+                }
+            } else {
+                const int rows = T / n;
+                const int l0 = t / n, m = t - l0 * n;
+                if (l0 < rows)
+                    for (int l = l0; l < R && g0 + l < nrow; l += rows) {
+                        const RowB rb = row_bases<DIM>(g0 + l, (int)tb, n, A.nl, A.wrap);
+                        double v[3];
+                        s1_cell<DIM>(A.s1, m, rb, n, v);
+                        const int off = tile_off<L>(l, m, TP);
+#pragma unroll
+                        for (int c = 0; c < NC; ++c) tile[c * RTP + off] = v[c];
+                    }
+            }
+        } else if (KIND == K_DIVPSI) {
+            // D.u at each cell for u^{n+1} and u^n
+            const unsigned stp[3] = {1u, N, N * N};
+            for_tile<AX>(n, nrow, R, g0, tb, t, T, [&](int l, int m, unsigned q) {
+                // cell coordinates along each axis: i = g0 + l; the line axis coordinate is m
+                int ijk[3];
+                ijk[0] = g0 + l;
+                if (AX == 1) { ijk[1] = m; ijk[2] = (int)tb; } else { ijk[1] = (int)tb; ijk[2] = m; }
+                double dn = 0.0, dol = 0.0;
+#pragma unroll
+                for (int c = 0; c < DIM; ++c) {
+                    const unsigned qp = (ijk[c] == n - 1) ? q - (N - 1) * stp[c] : q + stp[c];
+                    dn += ldg(A.unew[c] + qp) - ldg(A.unew[c] + q);
+                    dol += ldg(A.un[c] + qp) - ldg(A.un[c] + q);
+                }
+                dn *= A.invh;
+                dol *= A.invh;
+                tile[tile_off<L>(l, m, TP)] = A.neg_rho_dt * dn;         // Step 3e RHS
+                A.p[q] = A.p[q] - A.chimu_half * (dn + dol);             // Step 3f, explicit part
+            });
+        } else {
+            // pure copies: cp.async keeps every load of the tile in flight at once
+            const double* src = (KIND == K_PSI_LAST) ? A.pstar : pick3<double*>(A.io[0], A.io[1], A.io[2], comp);
+            const double* src2 = (KIND == K_LAST) ? pick3<const double*>(A.un[0], A.un[1], A.un[2], comp)
+                                                  : (KIND == K_PSI_LAST ? A.p : nullptr);
+            for_tile<AX>(n, nrow, R, g0, tb, t, T, [&](int l, int m, unsigned q) {
+                const int off = tile_off<L>(l, m, TP);
+                cp_async8(tile + off, src + q);
+                if (KIND == K_LAST || KIND == K_PSI_LAST) cp_async8(tile2 + off, src2 + q);
+            });
+            cp_async_wait_all();
+        }
+    }
+
+    // warp-synchronous solve of the tile's R lines (P lanes per line); w / nw: this
+    // warp's index among the nw warps that share the work
+    static __device__ __forceinline__ void solve(double* tile, const LineCoef& C, const double* sinvT, int R, int TP,
+                                                 int w, int nw)
+    {
+        const int P = C.P;
+        const unsigned RTP = (unsigned)R * TP;
+        const int lane = threadIdx.x & 31;
         const int lpw = (P <= 32) ? 32 / P : 1;          // lines per warp per round
         const int sub = lane / P;
         const int s = lane - sub * P;
@@ -422,31 +414,64 @@ __global__ void __launch_bounds__(256, MINB) k_lines(const LineCoef C, const Sch
             }
         }
     }
-    __syncthreads();
 
-    // ---------------- store (coalesced)
-    if (KIND == K_S1) {
-        for_tile<AX>(n, nrow, R, g0, tb, [&](int l, int m, unsigned q) {
-            const int off = tile_off<L>(l, m, TP);
+    // coalesced store of the solved tile (with the pass's epilogue)
+    static __device__ __forceinline__ void store(const double* tile, const double* tile2, const LArgs& A, int n, int R,
+                                                 int TP, int g0, unsigned tb, int comp, int t, int T)
+    {
+        const unsigned RTP = (unsigned)R * TP;
+        const int nrow = (DIM == 2) ? A.nl : n;
+        if (KIND == K_S1) {
+            for_tile<AX>(n, nrow, R, g0, tb, t, T, [&](int l, int m, unsigned q) {
+                const int off = tile_off<L>(l, m, TP);
 #pragma unroll
-            for (int c = 0; c < NC; ++c) A.s1.out[c][q] = tile[c * RTP + off];
-        });
-    } else {
-        double* dst = (KIND == K_PSI_LAST) ? A.pstar : pick3<double*>(A.io[0], A.io[1], A.io[2], comp);
-        for_tile<AX>(n, nrow, R, g0, tb, [&](int l, int m, unsigned q) {
-            const int off = tile_off<L>(l, m, TP);
-            if (KIND == K_LAST) {
-                dst[q] = tile2[off] + tile[off];            // u^{n+1} = u^n + d
-            } else if (KIND == K_PSI_LAST) {
-                const double psi = tile[off];
-                const double pn = tile2[off] + psi;        // Step 3f: p^{n+1/2} = q + psi^{n+1/2}
-                A.p[q] = pn;
-                dst[q] = pn + psi;                         // Step 3a of the next step: p* = p + psi
-            } else {
-                dst[q] = tile[off];
-            }
-        });
+                for (int c = 0; c < NC; ++c) A.s1.out[c][q] = tile[c * RTP + off];
+            });
+        } else {
+            double* dst = (KIND == K_PSI_LAST) ? A.pstar : pick3<double*>(A.io[0], A.io[1], A.io[2], comp);
+            for_tile<AX>(n, nrow, R, g0, tb, t, T, [&](int l, int m, unsigned q) {
+                const int off = tile_off<L>(l, m, TP);
+                if (KIND == K_LAST) {
+                    dst[q] = tile2[off] + tile[off];            // u^{n+1} = u^n + d
+                } else if (KIND == K_PSI_LAST) {
+                    const double psi = tile[off];
+                    const double pn = tile2[off] + psi;        // Step 3f: p^{n+1/2} = q + psi^{n+1/2}
+                    A.p[q] = pn;
+                    dst[q] = pn + psi;                         // Step 3a of the next step: p* = p + psi
+                } else {
+                    dst[q] = tile[off];
+                }
+            });
+        }
     }
+};
+
+__device__ __forceinline__ void load_sinvT(double* sinvT, const SchurInv* SI, int P)
+{
+    for (int e = threadIdx.x; e < P * P; e += blockDim.x) sinvT[e] = SI->sinvT[e];
+}
+
+// One tile per block, all threads in every phase (short grids; ib_line_solve).
+template <int L, int KIND, int DIM, int AX, int NC, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_lines(const LineCoef C, const SchurInv* __restrict__ SI, int n, int R,
+                                                     LArgs A)
+{
+    using LP = LinePass<L, KIND, DIM, AX, NC>;
+    extern __shared__ double smem[];
+    const int P = C.P;
+    const int TP = tile_pitch(P, L);
+    double* sinvT = smem;
+    double* tile = smem + P * P;
+    double* tile2 = tile + (size_t)NC * R * TP;   // LAST: u^n, PSI_LAST: q (prefetched with the fill)
+    load_sinvT(sinvT, SI, P);
+    const int comp = (NC == 1) ? blockIdx.z : 0;
+    const int g0 = blockIdx.x * R;
+    const unsigned tb = blockIdx.y;
+    LP::fill(tile, tile2, A, n, R, TP, g0, tb, comp, threadIdx.x, blockDim.x);
+    __syncthreads();
+    LP::solve(tile, C, sinvT, R, TP, threadIdx.x >> 5, blockDim.x >> 5);
+    __syncthreads();
+    LP::store(tile, tile2, A, n, R, TP, g0, tb, comp, threadIdx.x, blockDim.x);
 }
 
 __global__ void k_sub(const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ o, size_t cnt)
@@ -466,6 +491,12 @@ static int tiles_of(int kind, int nc) { return (kind == K_LAST || kind == K_PSI_
 // lines per block: the largest of {32, 16, 8} whose tile keeps >= 2 blocks per SM
 static int pick_r(const Ctx* s, int L, int nc)
 {
+    static int forced = -1;
+    if (forced < 0) {
+        const char* e = getenv("IBGM_R");
+        forced = e ? atoi(e) : 0;
+    }
+    if (forced == 8 || forced == 16 || forced == 32) return forced;
     for (int R = 32; R >= 8; R /= 2)
         if (lines_smem(s->P, L, nc, R) <= 100 * 1024) return R;
     return 8;
@@ -474,6 +505,13 @@ static int pick_r(const Ctx* s, int L, int nc)
 template <int L, int KIND, int DIM, int AX, int NC>
 static cudaError_t go_lines(Ctx* s, int sys, const LArgs& a, int ncomp_grid)
 {
+    // a pass along the last axis needs the whole line on this GPU
+    if (AX == DIM - 1 && !s->wrap) return cudaErrorInvalidValue;
+    LArgs la = a;
+    la.nl = (int)s->nl;
+    la.wrap = s->wrap;
+    const int64_t rows = (AX == 0 && DIM == 2) ? s->nl : s->n;
+    const int gy = (DIM == 3) ? (int)s->nl : 1;
     constexpr int MINB = (KIND == K_S1 || L >= 24) ? 2 : 4;
     auto kern = k_lines<L, KIND, DIM, AX, NC, MINB>;
     const int R = pick_r(s, L, tiles_of(KIND, NC));
@@ -484,13 +522,7 @@ static cudaError_t go_lines(Ctx* s, int sys, const LArgs& a, int ncomp_grid)
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    // a pass along the last axis needs the whole line on this GPU
-    if (AX == DIM - 1 && !s->wrap) return cudaErrorInvalidValue;
-    LArgs la = a;
-    la.nl = (int)s->nl;
-    la.wrap = s->wrap;
-    const int64_t rows = (AX == 0 && DIM == 2) ? s->nl : s->n;
-    dim3 grid((unsigned)((rows + R - 1) / R), (unsigned)((DIM == 3) ? s->nl : 1), (unsigned)ncomp_grid);
+    dim3 grid((unsigned)((rows + R - 1) / R), (unsigned)gy, (unsigned)ncomp_grid);
     kern<<<grid, 256, sm, s->stream>>>(s->hcoef[sys], s->sinv + sys, (int)s->n, R, la);
     s->launches++;
     return cudaGetLastError();

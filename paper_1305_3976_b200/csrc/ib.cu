@@ -2,6 +2,8 @@
 // of PAPER.md:577-621.  Lagrangian arrays are point-major [npts][dim].
 #include <cuda_runtime.h>
 
+#include <climits>
+
 #include "ibgm_internal.cuh"
 
 namespace ibgm {
@@ -418,6 +420,476 @@ __global__ void __launch_bounds__(256) k_brick_spread(
     }
 }
 
+// -------------------------------------------------------------------------------
+// Box-staged interpolation and spreading (Steps 1a and 2b).  The points are stored in
+// Morton order of their initial cells (ib_set_boundary), so the kBoxPts consecutive
+// points of a CTA lie close together: the CTA takes the bounding box of their 4-point
+// supports (all components), and
+//   interpolation  loads the box of u once (coalesced along x) into shared memory and
+//                  gathers each point's 4^d stencil from there;
+//   spreading      accumulates every contribution into the box in shared memory, then
+//                  adds the non-zero box entries into G (and f) with one global fp64
+//                  reduction each -- instead of 4^d d scattered global atomics per point.
+// Thread (p, c) owns point p of the chunk and velocity component c.  A chunk whose box
+// exceeds the shared-memory budget (points far apart) falls back to direct global
+// gathers / atomics for that chunk, so the result does not depend on the ordering.
+// -------------------------------------------------------------------------------
+constexpr int kBoxPts = 64;
+template <int DIM> struct BoxCap;
+template <> struct BoxCap<3> { static constexpr int EXT = 16, VOL = 2048; };
+template <> struct BoxCap<2> { static constexpr int EXT = 40, VOL = 1024; };
+
+// 1D weights with the UNWRAPPED base node index (base = floor(x) - 1)
+template <int KER>
+__device__ __forceinline__ void weights4u(double x, int& base, double w[4])
+{
+    const double fl = floor(x);
+    const double r = x - fl;
+    base = (int)fl - 1;
+    if (KER == IB_DELTA_COS4) {
+        double sn, cs;
+        sincospi(0.5 * r, &sn, &cs);
+        w[0] = 0.25 * (1.0 - sn);
+        w[1] = 0.25 * (1.0 + cs);
+        w[2] = 0.25 * (1.0 + sn);
+        w[3] = 0.25 * (1.0 - cs);
+    } else {
+        const double q = sqrt(1.0 + 4.0 * r - 4.0 * r * r);
+        w[0] = 0.125 * (3.0 - 2.0 * r - q);
+        w[1] = 0.125 * (3.0 - 2.0 * r + q);
+        w[2] = 0.125 * (1.0 + 2.0 * r + q);
+        w[3] = 0.125 * (1.0 + 2.0 * r - q);
+    }
+}
+
+__device__ __forceinline__ int wrapm(int i, int n)
+{
+    i %= n;
+    return i < 0 ? i + n : i;
+}
+
+// chunk box: origin o (unwrapped node index) and extents e per axis; false if it does
+// not fit.  Every thread of the CTA must call it (two barriers).
+template <int DIM>
+__device__ __forceinline__ bool chunk_box(const double* Xk, bool lead, double invh, int* sh, int o[3], int e[3], int& V)
+{
+    if (threadIdx.x < 3) { sh[threadIdx.x] = INT_MAX; sh[3 + threadIdx.x] = INT_MIN; }
+    __syncthreads();
+    if (lead)
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) {
+            const int ci = (int)floor(Xk[a] * invh);
+            atomicMin(sh + a, ci);
+            atomicMax(sh + 3 + a, ci);
+        }
+    __syncthreads();
+    bool ok = true;
+    V = 1;
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) {
+        o[a] = sh[a] - 2;
+        e[a] = sh[3 + a] - sh[a] + 5;
+        ok = ok && e[a] <= BoxCap<DIM>::EXT;
+        V *= e[a];
+    }
+    return ok && V <= BoxCap<DIM>::VOL;
+}
+
+// Walk the box row by row: XL lanes along x (no per-element division), rows (c, y[, z])
+// spread over the remaining lanes.  f(c, i, q): i the box index, q the global index.
+template <int DIM, class Fn>
+__device__ __forceinline__ void for_box(const int o[3], const int e[3], int V, int n, Fn&& f)
+{
+    constexpr int XL = (DIM == 3) ? 16 : 32;
+    const int xl = threadIdx.x % XL, rstep = blockDim.x / XL;
+    const int rows_c = (DIM == 3) ? e[1] * e[2] : e[1];
+    const int ox = wrapm(o[0], n);
+    const size_t nn = (size_t)n;
+    for (int r = threadIdx.x / XL; r < DIM * rows_c; r += rstep) {
+        const int c = r / rows_c;
+        const int rr = r - c * rows_c;
+        const int z = (DIM == 3) ? rr / e[1] : 0;
+        const int y = rr - z * e[1];
+        size_t rowg = nn * (size_t)wrapm(o[1] + y, n);
+        if (DIM == 3) rowg += nn * nn * (size_t)wrapm(o[2] + z, n);
+        const int rowb = c * V + (z * e[1] + y) * e[0];
+        for (int x = xl; x < e[0]; x += XL) {
+            int gx = ox + x;
+            while (gx >= n) gx -= n;
+            f(c, rowb + x, rowg + (size_t)gx);
+        }
+    }
+}
+
+template <int DIM, int KER>
+__global__ void __launch_bounds__(kBoxPts * DIM) k_interp_box(const double* __restrict__ u0, const double* __restrict__ u1,
+                                                            const double* __restrict__ u2, double* __restrict__ X,
+                                                            double* __restrict__ Xh, double* __restrict__ Uprev,
+                                                            int64_t npts, int n, double invh, double dt, int first)
+{
+    extern __shared__ double box[];
+    __shared__ int sh[6];
+    const int t = threadIdx.x;
+    const int p = t % kBoxPts, c = t / kBoxPts;
+    const int64_t k = blockIdx.x * (int64_t)kBoxPts + p;
+    const bool valid = k < npts;
+    double Xk[3] = {0, 0, 0};
+    if (valid)
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) Xk[a] = X[k * DIM + a];
+    int o[3] = {0, 0, 0}, e[3] = {1, 1, 1}, V;
+    const bool fits = chunk_box<DIM>(Xk, valid && c == 0, invh, sh, o, e, V);
+    if (fits) {
+        for_box<DIM>(o, e, V, n, [&](int cc, int i, size_t q) {
+            const double* ucc = (cc == 0) ? u0 : (cc == 1 ? u1 : u2);
+            box[i] = __ldg(ucc + q);
+        });
+        __syncthreads();
+    }
+    if (!valid) return;
+    int b[3] = {0, 0, 0};
+    double w[3][4];
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) weights4u<KER>(Xk[a] * invh - (a == c ? 0.0 : 0.5), b[a], w[a]);
+    double acc = 0.0;
+    if (fits) {
+        const double* bc = box + c * V;
+        if (DIM == 2) {
+#pragma unroll
+            for (int m1 = 0; m1 < 4; ++m1) {
+                const double* row = bc + (b[1] - o[1] + m1) * e[0] + (b[0] - o[0]);
+                double r = 0.0;
+#pragma unroll
+                for (int m0 = 0; m0 < 4; ++m0) r += w[0][m0] * row[m0];
+                acc += w[1][m1] * r;
+            }
+        } else {
+#pragma unroll
+            for (int m2 = 0; m2 < 4; ++m2) {
+                double pa = 0.0;
+#pragma unroll
+                for (int m1 = 0; m1 < 4; ++m1) {
+                    const double* row = bc + ((b[2] - o[2] + m2) * e[1] + (b[1] - o[1] + m1)) * e[0] + (b[0] - o[0]);
+                    double r = 0.0;
+#pragma unroll
+                    for (int m0 = 0; m0 < 4; ++m0) r += w[0][m0] * row[m0];
+                    pa += w[1][m1] * r;
+                }
+                acc += w[2][m2] * pa;
+            }
+        }
+    } else {
+        const double* u = (c == 0) ? u0 : (c == 1 ? u1 : u2);
+        const size_t nn = (size_t)n;
+        if (DIM == 2) {
+#pragma unroll
+            for (int m1 = 0; m1 < 4; ++m1) {
+                const size_t row = nn * (size_t)wrapm(b[1] + m1, n);
+                double r = 0.0;
+#pragma unroll
+                for (int m0 = 0; m0 < 4; ++m0) r += w[0][m0] * u[row + wrapm(b[0] + m0, n)];
+                acc += w[1][m1] * r;
+            }
+        } else {
+#pragma unroll
+            for (int m2 = 0; m2 < 4; ++m2) {
+                const size_t pl = nn * nn * (size_t)wrapm(b[2] + m2, n);
+                double pa = 0.0;
+#pragma unroll
+                for (int m1 = 0; m1 < 4; ++m1) {
+                    const size_t row = pl + nn * (size_t)wrapm(b[1] + m1, n);
+                    double r = 0.0;
+#pragma unroll
+                    for (int m0 = 0; m0 < 4; ++m0) r += w[0][m0] * u[row + wrapm(b[0] + m0, n)];
+                    pa += w[1][m1] * r;
+                }
+                acc += w[2][m2] * pa;
+            }
+        }
+    }
+    // Steps 1b-1c for component c of this point
+    const double xc = (c == 0) ? Xk[0] : (c == 1 ? Xk[1] : Xk[2]);
+    const double up = Uprev[k * DIM + c];
+    const double xn = first ? xc + dt * acc : xc + dt * (1.5 * acc - 0.5 * up);
+    Xh[k * DIM + c] = 0.5 * (xn + xc);
+    X[k * DIM + c] = xn;
+    Uprev[k * DIM + c] = acc;
+}
+
+// shared layout of the spread: box [DIM][VOL], then per (component, point) the weights
+// [DIM axes][4] and the scaled force; the box-relative base nodes are static shared
+template <int DIM>
+__host__ __device__ constexpr size_t spread_box_doubles()
+{
+    return (size_t)DIM * (DIM == 3 ? BoxCap<3>::VOL : BoxCap<2>::VOL) + (size_t)DIM * kBoxPts * (DIM * 4 + 1);
+}
+
+template <int DIM, int KER, bool KEEP>
+__global__ void __launch_bounds__(kBoxPts * DIM) k_spread_box(const double* __restrict__ Xh, const double* __restrict__ F,
+                                                            const double* __restrict__ wgt, double* __restrict__ g0,
+                                                            double* __restrict__ g1, double* __restrict__ g2,
+                                                            double* __restrict__ f0, double* __restrict__ f1,
+                                                            double* __restrict__ f2, int64_t npts, int n, double invh,
+                                                            double invhd, double two_rho)
+{
+    constexpr int VOL = (DIM == 3) ? BoxCap<3>::VOL : BoxCap<2>::VOL;
+    extern __shared__ double box[];
+    double* W = box + DIM * VOL;                      // [c][p][a][4]
+    double* coef = W + DIM * kBoxPts * DIM * 4;       // [c][p]
+    __shared__ int sh[6];
+    __shared__ int bs[DIM * kBoxPts * 4];             // [c][p][a] (padded to 4)
+    const int t = threadIdx.x;
+    const int p = t % kBoxPts, c = t / kBoxPts;
+    const int64_t k = blockIdx.x * (int64_t)kBoxPts + p;
+    const bool valid = k < npts;
+    double Xk[3] = {0, 0, 0};
+    if (valid)
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) Xk[a] = Xh[k * DIM + a];
+    int o[3] = {0, 0, 0}, e[3] = {1, 1, 1}, V;
+    const bool fits = chunk_box<DIM>(Xk, valid && c == 0, invh, sh, o, e, V);
+    double* gcc = (c == 0) ? g0 : (c == 1 ? g1 : g2);
+    double* fcc = (c == 0) ? f0 : (c == 1 ? f1 : f2);
+    int b[3] = {0, 0, 0};
+    double w[3][4];
+    double Fc = 0.0;
+    if (valid) {
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) weights4u<KER>(Xk[a] * invh - (a == c ? 0.0 : 0.5), b[a], w[a]);
+        Fc = F[k * DIM + c] * wgt[k] * invhd;
+    }
+    if (!fits) {
+        // direct fallback: 4^d global reductions for this (point, component)
+        if (!valid) return;
+        const size_t nn = (size_t)n;
+        if (DIM == 2) {
+#pragma unroll
+            for (int m1 = 0; m1 < 4; ++m1) {
+                const size_t row = nn * (size_t)wrapm(b[1] + m1, n);
+                const double a1 = Fc * w[1][m1];
+#pragma unroll
+                for (int m0 = 0; m0 < 4; ++m0) {
+                    const size_t q = row + wrapm(b[0] + m0, n);
+                    const double v = a1 * w[0][m0];
+                    atomicAdd(gcc + q, two_rho * v);
+                    if (KEEP) atomicAdd(fcc + q, v);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int m2 = 0; m2 < 4; ++m2) {
+                const size_t pl = nn * nn * (size_t)wrapm(b[2] + m2, n);
+                const double a2 = Fc * w[2][m2];
+#pragma unroll
+                for (int m1 = 0; m1 < 4; ++m1) {
+                    const size_t row = pl + nn * (size_t)wrapm(b[1] + m1, n);
+                    const double a1 = a2 * w[1][m1];
+#pragma unroll
+                    for (int m0 = 0; m0 < 4; ++m0) {
+                        const size_t q = row + wrapm(b[0] + m0, n);
+                        const double v = a1 * w[0][m0];
+                        atomicAdd(gcc + q, two_rho * v);
+                        if (KEEP) atomicAdd(fcc + q, v);
+                    }
+                }
+            }
+        }
+        return;
+    }
+    // per (component, point): box-relative base nodes, weights, scaled force
+    {
+        const int cp = c * kBoxPts + p;
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) {
+            bs[cp * 4 + a] = valid ? b[a] - o[a] : -1000;
+#pragma unroll
+            for (int m = 0; m < 4; ++m) W[(cp * DIM + a) * 4 + m] = w[a][m];
+        }
+        coef[cp] = Fc;
+    }
+    for (int i = t; i < DIM * V; i += blockDim.x) box[i] = 0.0;
+    __syncthreads();
+    // owner accumulation (no atomics): a thread owns a z-column (c, x, y) of the box in
+    // 3D (a node (c, x, y) in 2D) and adds every point of the chunk whose support covers it
+    const int plane = e[0] * e[1];
+    for (int col = t; col < DIM * plane; col += blockDim.x) {
+        const int cc = col / plane;
+        const int rem = col - cc * plane;
+        const int y = rem / e[0];
+        const int x = rem - y * e[0];
+        double* colp = box + cc * V + rem;
+        const int* bsc = bs + cc * kBoxPts * 4;
+        const double* Wc = W + cc * kBoxPts * DIM * 4;
+        const double* cfc = coef + cc * kBoxPts;
+        double acc2 = 0.0;
+        for (int q = 0; q < kBoxPts; ++q) {
+            const int dx = x - bsc[q * 4], dy = y - bsc[q * 4 + 1];
+            if ((unsigned)dx < 4u && (unsigned)dy < 4u) {
+                const double* wq = Wc + q * DIM * 4;
+                const double v = cfc[q] * wq[dx] * wq[4 + dy];
+                if (DIM == 3) {
+                    double* zp = colp + bsc[q * 4 + 2] * plane;
+#pragma unroll
+                    for (int dz = 0; dz < 4; ++dz) zp[dz * plane] += v * wq[8 + dz];
+                } else {
+                    acc2 += v;
+                }
+            }
+        }
+        if (DIM == 2) *colp = acc2;
+    }
+    __syncthreads();
+    for_box<DIM>(o, e, V, n, [&](int cc, int i, size_t q) {
+        const double v = box[i];
+        if (v == 0.0) return;
+        atomicAdd(((cc == 0) ? g0 : (cc == 1 ? g1 : g2)) + q, two_rho * v);
+        if (KEEP) atomicAdd(((cc == 0) ? f0 : (cc == 1 ? f1 : f2)) + q, v);
+    });
+}
+
+// -------------------------------------------------------------------------------
+// Quad-lane interpolation and spreading (Steps 1a, 2b): 4 lanes per (point,
+// component), lane m0 owns the stencil nodes i0+m0 along x, so one warp instruction
+// touches 8 rows of 4 consecutive nodes (coalesced sectors) instead of 32 scattered
+// nodes.  Groups of a warp are 8 consecutive points (Morton order) of one component.
+// -------------------------------------------------------------------------------
+template <int DIM, int KER>
+__device__ __forceinline__ void quad_weights(const double* Xk, int c, double invh, int n, int b[3], double w[3][4])
+{
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) {
+        weights4u<KER>(Xk[a] * invh - (a == c ? 0.0 : 0.5), b[a], w[a]);
+        b[a] = wrapm(b[a], n);
+    }
+}
+
+template <int DIM, int KER>
+__global__ void __launch_bounds__(256) k_interp_quad(const double* __restrict__ u0, const double* __restrict__ u1,
+                                                     const double* __restrict__ u2, double* __restrict__ X,
+                                                     double* __restrict__ Xh, double* __restrict__ Uprev,
+                                                     int64_t npts, int n, double invh, double dt, int first)
+{
+    const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 2;   // (component, point) group
+    const int m0 = threadIdx.x & 3;
+    // groups ordered (point block of 8, component, point): a warp = 8 points x 1 component
+    const int64_t blk = g / (8 * DIM);
+    const int rem = (int)(g - blk * 8 * DIM);
+    const int c = rem >> 3;
+    const int64_t k = blk * 8 + (rem & 7);
+    const bool valid = k < npts;
+    double Xk[3] = {0, 0, 0};
+    const int64_t kk = valid ? k : 0;
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) Xk[a] = X[kk * DIM + a];
+    int b[3];
+    double w[3][4];
+    quad_weights<DIM, KER>(Xk, c, invh, n, b, w);
+    const double* u = (c == 0) ? u0 : (c == 1 ? u1 : u2);
+    int ix = b[0] + m0;
+    if (ix >= n) ix -= n;
+    const double wx = (m0 == 0) ? w[0][0] : (m0 == 1 ? w[0][1] : (m0 == 2 ? w[0][2] : w[0][3]));
+    const size_t nn = (size_t)n;
+    double acc = 0.0;
+    if (DIM == 2) {
+#pragma unroll
+        for (int m1 = 0; m1 < 4; ++m1) {
+            int iy = b[1] + m1;
+            if (iy >= n) iy -= n;
+            acc += w[1][m1] * __ldg(u + nn * iy + ix);
+        }
+    } else {
+#pragma unroll
+        for (int m2 = 0; m2 < 4; ++m2) {
+            int iz = b[2] + m2;
+            if (iz >= n) iz -= n;
+            double pa = 0.0;
+#pragma unroll
+            for (int m1 = 0; m1 < 4; ++m1) {
+                int iy = b[1] + m1;
+                if (iy >= n) iy -= n;
+                pa += w[1][m1] * __ldg(u + nn * (nn * iz + iy) + ix);
+            }
+            acc += w[2][m2] * pa;
+        }
+    }
+    acc *= wx;
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    if (!valid || m0 != 0) return;
+    const double xc = (c == 0) ? Xk[0] : (c == 1 ? Xk[1] : Xk[2]);
+    const double up = Uprev[k * DIM + c];
+    const double xn = first ? xc + dt * acc : xc + dt * (1.5 * acc - 0.5 * up);
+    Xh[k * DIM + c] = 0.5 * (xn + xc);
+    X[k * DIM + c] = xn;
+    Uprev[k * DIM + c] = acc;
+}
+
+template <int DIM, int KER, bool KEEP>
+__global__ void __launch_bounds__(256) k_spread_quad(const double* __restrict__ Xh, const double* __restrict__ F,
+                                                     const double* __restrict__ wgt, double* __restrict__ g0,
+                                                     double* __restrict__ g1, double* __restrict__ g2,
+                                                     double* __restrict__ f0, double* __restrict__ f1,
+                                                     double* __restrict__ f2, int64_t npts, int n, double invh,
+                                                     double invhd, double two_rho)
+{
+    const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 2;
+    const int m0 = threadIdx.x & 3;
+    const int64_t blk = g / (8 * DIM);
+    const int rem = (int)(g - blk * 8 * DIM);
+    const int c = rem >> 3;
+    const int64_t k = blk * 8 + (rem & 7);
+    if (k >= npts) return;
+    double Xk[3] = {0, 0, 0};
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) Xk[a] = Xh[k * DIM + a];
+    int b[3];
+    double w[3][4];
+    quad_weights<DIM, KER>(Xk, c, invh, n, b, w);
+    double* gc = (c == 0) ? g0 : (c == 1 ? g1 : g2);
+    double* fc = (c == 0) ? f0 : (c == 1 ? f1 : f2);
+    int ix = b[0] + m0;
+    if (ix >= n) ix -= n;
+    const double wx = (m0 == 0) ? w[0][0] : (m0 == 1 ? w[0][1] : (m0 == 2 ? w[0][2] : w[0][3]));
+    const double Fx = F[k * DIM + c] * wgt[k] * invhd * wx;
+    const size_t nn = (size_t)n;
+    if (DIM == 2) {
+#pragma unroll
+        for (int m1 = 0; m1 < 4; ++m1) {
+            int iy = b[1] + m1;
+            if (iy >= n) iy -= n;
+            const double v = Fx * w[1][m1];
+            atomicAdd(gc + nn * iy + ix, two_rho * v);
+            if (KEEP) atomicAdd(fc + nn * iy + ix, v);
+        }
+    } else {
+#pragma unroll
+        for (int m2 = 0; m2 < 4; ++m2) {
+            int iz = b[2] + m2;
+            if (iz >= n) iz -= n;
+            const double a2 = Fx * w[2][m2];
+#pragma unroll
+            for (int m1 = 0; m1 < 4; ++m1) {
+                int iy = b[1] + m1;
+                if (iy >= n) iy -= n;
+                const double v = a2 * w[1][m1];
+                const size_t q = nn * (nn * iz + iy) + ix;
+                atomicAdd(gc + q, two_rho * v);
+                if (KEEP) atomicAdd(fc + q, v);
+            }
+        }
+    }
+}
+
+// dst[idx[i]] = src[i] per point (internal -> caller order)
+__global__ void k_scatter_pts(const double* __restrict__ src, const int32_t* __restrict__ idx, double* __restrict__ dst,
+                              int64_t npts, int dim)
+{
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= npts * dim) return;
+    const int64_t k = e / dim;
+    dst[(int64_t)idx[k] * dim + (e - k * dim)] = src[e];
+}
+
 __global__ void k_check_finite(const double* __restrict__ a, size_t cnt, int* __restrict__ flag)
 {
     for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < cnt; q += (size_t)gridDim.x * blockDim.x)
@@ -426,9 +898,56 @@ __global__ void k_check_finite(const double* __restrict__ a, size_t cnt, int* __
 
 static unsigned nblk(int64_t cnt, int thr) { return (unsigned)((cnt + thr - 1) / thr); }
 
+static size_t box_smem(int dim) { return (size_t)dim * (dim == 3 ? BoxCap<3>::VOL : BoxCap<2>::VOL) * sizeof(double); }
+static size_t spread_smem(int dim)
+{
+    return (dim == 3 ? spread_box_doubles<3>() : spread_box_doubles<2>()) * sizeof(double);
+}
+
+// opt in to the box's dynamic shared memory once per kernel instantiation (ID tells the
+// instantiations apart: they share one function type)
+template <int ID, class K>
+static cudaError_t box_attr(K kern, size_t sm)
+{
+    static bool done = false;
+    if (done) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e == cudaSuccess) done = true;
+    return e;
+}
+
 cudaError_t launch_interp_evolve(Ctx* s, int first)
 {
     if (s->npts == 0) return cudaSuccess;
+    if (s->interp_mode == 3) {
+        const int64_t thr = ((s->npts + 7) / 8) * 8 * s->dim * 4;
+        const unsigned nbk = (unsigned)((thr + 255) / 256);
+        const double invh = 1.0 / s->h;
+#define IBGM_IQ(D, K) k_interp_quad<D, K><<<nbk, 256, 0, s->stream>>>(s->u[0], s->u[1], s->u[2], s->X, s->Xh, \
+                                                                      s->Uprev, s->npts, (int)s->n, invh, s->dt, first)
+        if (s->dim == 2) { if (s->kernel == IB_DELTA_COS4) IBGM_IQ(2, 0); else IBGM_IQ(2, 1); }
+        else { if (s->kernel == IB_DELTA_COS4) IBGM_IQ(3, 0); else IBGM_IQ(3, 1); }
+#undef IBGM_IQ
+        s->launches++;
+        return cudaGetLastError();
+    }
+    if (s->interp_mode == 2) {
+        const unsigned nbk = (unsigned)((s->npts + kBoxPts - 1) / kBoxPts);
+        const size_t sm = box_smem(s->dim);
+        const double invh = 1.0 / s->h;
+#define IBGM_IB(D, K)                                                                                   \
+    do {                                                                                                \
+        const cudaError_t ae_ = box_attr<10 * D + K>(k_interp_box<D, K>, sm);                                         \
+        if (ae_ != cudaSuccess) return ae_;                                                             \
+        k_interp_box<D, K><<<nbk, kBoxPts * D, sm, s->stream>>>(s->u[0], s->u[1], s->u[2], s->X, s->Xh, \
+                                                                    s->Uprev, s->npts, (int)s->n, invh, s->dt, first); \
+    } while (0)
+        if (s->dim == 2) { if (s->kernel == IB_DELTA_COS4) IBGM_IB(2, 0); else IBGM_IB(2, 1); }
+        else { if (s->kernel == IB_DELTA_COS4) IBGM_IB(3, 0); else IBGM_IB(3, 1); }
+#undef IBGM_IB
+        s->launches++;
+        return cudaGetLastError();
+    }
     const int thr = 128;
     const double invh = 1.0 / s->h;
 #define IBGM_IE(D, K) k_interp_evolve<D, K><<<nblk(s->npts, thr), thr, 0, s->stream>>>( \
@@ -509,11 +1028,71 @@ static cudaError_t launch_spread_direct(Ctx* s)
     return cudaGetLastError();
 }
 
+static cudaError_t launch_spread_box(Ctx* s)
+{
+    const unsigned nbk = (unsigned)((s->npts + kBoxPts - 1) / kBoxPts);
+    const size_t sm = spread_smem(s->dim);
+    const double invh = 1.0 / s->h;
+    const double invhd = (s->dim == 3) ? invh * invh * invh : invh * invh;
+    const double two_rho = 2.0 / s->rho;
+#define IBGM_SB(D, K, KP)                                                                                  \
+    do {                                                                                                   \
+        const cudaError_t ae_ = box_attr<100 + 10 * D + 2 * K + KP>(k_spread_box<D, K, KP>, sm);                                      \
+        if (ae_ != cudaSuccess) return ae_;                                                                \
+        k_spread_box<D, K, KP><<<nbk, kBoxPts * D, sm, s->stream>>>(s->Xh, s->F, s->wgt, s->nprev[0],   \
+                s->nprev[1], s->nprev[2], s->f[0], s->f[1], s->f[2], s->npts, (int)s->n, invh, invhd, two_rho); \
+    } while (0)
+    const bool kp = s->debug_keep_f != 0;
+    if (s->dim == 2) {
+        if (s->kernel == IB_DELTA_COS4) { if (kp) IBGM_SB(2, 0, true); else IBGM_SB(2, 0, false); }
+        else { if (kp) IBGM_SB(2, 1, true); else IBGM_SB(2, 1, false); }
+    } else {
+        if (s->kernel == IB_DELTA_COS4) { if (kp) IBGM_SB(3, 0, true); else IBGM_SB(3, 0, false); }
+        else { if (kp) IBGM_SB(3, 1, true); else IBGM_SB(3, 1, false); }
+    }
+#undef IBGM_SB
+    s->launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scatter_pts(Ctx* s, const double* src, double* dst)
+{
+    const int64_t cnt = s->npts * s->dim;
+    if (cnt == 0) return cudaSuccess;
+    k_scatter_pts<<<nblk(cnt, 256), 256, 0, s->stream>>>(src, s->pt_user, dst, s->npts, s->dim);
+    s->launches++;
+    return cudaGetLastError();
+}
+
+static cudaError_t launch_spread_quad(Ctx* s)
+{
+    const int64_t thr = ((s->npts + 7) / 8) * 8 * s->dim * 4;
+    const unsigned nbk = (unsigned)((thr + 255) / 256);
+    const double invh = 1.0 / s->h;
+    const double invhd = (s->dim == 3) ? invh * invh * invh : invh * invh;
+    const double two_rho = 2.0 / s->rho;
+#define IBGM_SQ(D, K, KP) k_spread_quad<D, K, KP><<<nbk, 256, 0, s->stream>>>(s->Xh, s->F, s->wgt, s->nprev[0], \
+        s->nprev[1], s->nprev[2], s->f[0], s->f[1], s->f[2], s->npts, (int)s->n, invh, invhd, two_rho)
+    const bool kp = s->debug_keep_f != 0;
+    if (s->dim == 2) {
+        if (s->kernel == IB_DELTA_COS4) { if (kp) IBGM_SQ(2, 0, true); else IBGM_SQ(2, 0, false); }
+        else { if (kp) IBGM_SQ(2, 1, true); else IBGM_SQ(2, 1, false); }
+    } else {
+        if (s->kernel == IB_DELTA_COS4) { if (kp) IBGM_SQ(3, 0, true); else IBGM_SQ(3, 0, false); }
+        else { if (kp) IBGM_SQ(3, 1, true); else IBGM_SQ(3, 1, false); }
+    }
+#undef IBGM_SQ
+    s->launches++;
+    return cudaGetLastError();
+}
+
 cudaError_t launch_spread(Ctx* s)
 {
     if (s->npts == 0) return cudaSuccess;
-    // direct per-point atomics below ~3e5 points (cheaper than binning); bricks above
-    if (s->spread_mode == 1 || (s->spread_mode == 0 && s->npts < 300000)) return launch_spread_direct(s);
+    // 0 (auto) and 4: quad-lane atomics; 1: per-point atomics; 2: brick-binned; 3: box-staged
+    if (s->spread_mode == 0 || s->spread_mode == 4) return launch_spread_quad(s);
+    if (s->spread_mode == 3) return launch_spread_box(s);
+    if (s->spread_mode == 1) return launch_spread_direct(s);
     const int thr = 256;
     const double invh = 1.0 / s->h;
     cudaError_t e = cudaMemsetAsync(s->bin_count, 0, sizeof(int) * s->nbricks, s->stream);

@@ -23,6 +23,7 @@ struct LineCoef {
     double c, a, b;
     double inv_rowsum;        // 1/(a+b+c): mean(x) = mean(d)/(a+b+c) for circulant A
     double gsum, hsum;        // sum_i g_i, sum_i h_i
+    double inv_n;             // 1/N
     int L, P, N, mean_fix;
     double inv[kMaxL];        // Thomas: 1/den_i of B (i = 0..m-1)
     double cp[kMaxL];         // Thomas: b/den_i
@@ -33,6 +34,7 @@ struct LineCoef {
 // dense inverse of the P x P periodic Schur matrix S and its column sums (device)
 struct SchurInv {
     double sinv[kMaxSeg * kMaxSeg];
+    double sinvT[kMaxSeg * kMaxSeg];  // transposed: sinvT[q P + p] = sinv[p P + q]
     double colsum[kMaxSeg];
 };
 
@@ -79,7 +81,11 @@ struct Ctx {
     int64_t nbricks;
     int *bin_bid, *bin_count, *bin_start, *bin_cursor, *bin_list, *bin_nlist, *bin_sorted, *bin_partial;
     int debug_keep_f;                 // ib_set_debug: also accumulate f for ib_get_aux
-    int spread_mode;                  // 0 auto, 1 direct atomics, 2 brick-binned (ib_set_debug bits 1-2)
+    int spread_mode;                  // ib_set_debug bits 1-3: 0 auto (quad), 1 per-point, 2 brick, 3 box, 4 quad
+    int interp_mode;                  // ib_set_debug bits 4-5: 0 auto (per-point), 1 per-point, 2 box, 3 quad
+    // internal point order (Morton order of the initial cells): pt_user[i] = caller index
+    int32_t* pt_user;
+    double* lag_tmp;                  // [npts][dim] scratch for returning points in caller order
     int64_t step;                     // steps completed since set_fields/set_boundary
     bool fields_set;
     int64_t launches;
@@ -166,5 +172,6 @@ cudaError_t launch_interp_evolve(Ctx* s, int first_step);    // Steps 1a-1c
 cudaError_t launch_force(Ctx* s);                            // Step 2a
 cudaError_t launch_spread(Ctx* s);                           // Step 2b (into G, and f in debug mode)
 cudaError_t launch_check_finite(Ctx* s);
+cudaError_t launch_scatter_pts(Ctx* s, const double* src, double* dst);   // internal -> caller order
 
 }  // namespace ibgm

@@ -143,7 +143,7 @@ class Context:
         L = lib()
         self.dim, self.n = dim, n
         self.nranks, self.rank, self.transport = nranks, rank, transport
-        self.local = nranks > 1 and transport == IB_TRANSPORT_NCCL
+        self.local = nranks > 1 and transport == IB_TRANSPORT_NCCL   # fields are this rank's slab
         self.nz = n // nranks if self.local else n
         g = ib_grid(dim, n, 1.0)
         o = ib_options()
@@ -241,9 +241,10 @@ class Context:
     def check_finite(self):
         _ck(lib().ib_check_finite(self._h))
 
-    def set_debug(self, keep_f: bool, spread_mode: int = 0):
-        """keep_f: keep f^{n+1/2} for aux(); spread_mode: 0 auto, 1 per-point atomics, 2 brick-binned."""
-        _ck(lib().ib_set_debug(self._h, int(keep_f) | (int(spread_mode) << 1)))
+    def set_debug(self, keep_f: bool, spread_mode: int = 0, interp_mode: int = 0):
+        """keep_f: keep f^{n+1/2} for aux(); spread_mode: 0 auto, 1 per-point, 2 brick-binned,
+        3 box-staged, 4 quad-lane; interp_mode: 0 auto, 1 per-point, 2 box-staged, 3 quad-lane."""
+        _ck(lib().ib_set_debug(self._h, int(keep_f) | (int(spread_mode) << 1) | (int(interp_mode) << 4)))
 
     def set_profiling(self, on: bool):
         _ck(lib().ib_set_profiling(self._h, int(on)))

@@ -160,3 +160,30 @@ def test_nccl_unique_id_loads_on_the_gpu_box():
     from paper_1305_3976_b200 import ibgm
     a, b = ibgm.nccl_unique_id(), ibgm.nccl_unique_id()
     assert len(a) == 128 and a != b
+
+
+@pytest.mark.parametrize("transport", ["nccl", "emulate"])
+def test_one_slab_transports(transport):
+    """One slab through the slab code path: the NCCL transport on a 1-rank communicator
+    (self send/recv carries the periodic halo; all-gather/all-reduce of size 1, captured
+    in the step's CUDA graph) and EMULATE with P = 1; both vs the oracle and the
+    single-GPU path."""
+    from paper_1305_3976_b200 import ibgm, inputs
+    pr = inputs.config(3, n=32, nodes=2000)
+    if transport == "nccl":
+        g = ibgm.from_problem(pr, nranks=1, rank=0, nccl_id=ibgm.nccl_unique_id())
+    else:
+        g = ibgm.from_problem(pr, nranks=1, transport=EMU)
+    g1 = _gpu(pr, 1)
+    o = _oracle_for(pr)
+    o.step(10); g.step(10); g1.step(10)
+    fo, fg, f1 = o.fields(), g.fields(), g1.fields()
+    for c in range(3):
+        assert _rel(fg["u"][c], fo["u"][c]) <= 1e-9
+        assert _rel(fg["u"][c], f1["u"][c]) <= 1e-10
+    assert _rel(fg["p"], fo["p"]) <= 1e-9 and _rel(fg["X"], fo["X"]) <= 1e-9
+    d = RNG.standard_normal((32, 32, 32))
+    x = g.line_solve(2, 32.0 ** 2, d)
+    from oracle import oracle as O
+    assert _rel(x, O.solve_axis(d, 2, -1024.0, 2049.0, -1024.0)) <= 1e-12
+    g.close(); g1.close()

@@ -14,6 +14,7 @@ ALG = {3: {"s1_rhs_xsweep": 13, "sweep_y": 6, "sweep_z": 9, "div_psi_first": 9, 
 
 
 MODE = int(os.environ.get("SPREAD_MODE", "0"))
+IMODE = int(os.environ.get("INTERP_MODE", "0"))
 
 
 def run(cfg, steps=50, **over):
@@ -23,7 +24,7 @@ def run(cfg, steps=50, **over):
     st = torch.cuda.Stream()
     torch.cuda.set_stream(st)
     ctx = ibgm.from_problem(pr, stream=st.cuda_stream)
-    ctx.set_debug(False, MODE)
+    ctx.set_debug(False, MODE, IMODE)
     ctx.step(5)
     ctx.sync()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
