@@ -217,6 +217,13 @@ class Context:
                                 _p(X) if self.npts else None, _p(U) if self.npts else None))
         return dict(u=u, p=p, psi=psi, X=X, U=U)
 
+    def positions(self):
+        """X^n only ([npts][dim], caller's point order)."""
+        X = np.empty((self.npts, self.dim))
+        if self.npts:
+            _ck(lib().ib_get_fields(self._h, None, None, None, None, None, _p(X), None))
+        return X
+
     def get_fields_into(self, u, v, w, p, X):
         """D2H into caller buffers (e.g. pinned); any may be None."""
         _ck(lib().ib_get_fields(self._h, _p(u), _p(v), _p(w), _p(p), None, _p(X), None))

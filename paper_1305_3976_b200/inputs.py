@@ -158,6 +158,77 @@ def random_divfree(dim: int, n: int, K: int, amp: float, seed: int):
     return [np.ascontiguousarray(c * (amp / m)) for c in u]
 
 
+# ------------------------------------------------------------------ the paper's own problems
+# (validation and timing workloads of PAPER.md section 5)
+def thin_ellipse(n: int, sigma: float = 1.0, dt: float = 0.04 / 512, mu: float = 0.01) -> Problem:
+    """Thin ellipse of PAPER.md:1294-1345: r1 = 5/28, r2 = 7/20 centred at (1/2, 1/2),
+    N_s = 19N/4 points uniform in s, stiffness sigma, rest length 0, fluid at rest,
+    mu = 0.01, rho = 1, the paper's delta kernel (eq. discretedelta)."""
+    ns = 19 * n // 4
+    pr = Problem(f"thin_ellipse_n{n}", 2, n, mu, 1.0, dt, 0, kernel=PESKIN4)
+    pr.u = [np.zeros((n, n)), np.zeros((n, n))]
+    pr.p = np.zeros((n, n))
+    pr.X, pr.edges, pr.kappa, pr.weight = ellipse_fibre(ns, (0.5, 0.5), (5.0 / 28.0, 7.0 / 20.0), sigma)
+    return pr
+
+
+def thick_shell(n: int, mu: float = 0.01, dt: float = 0.08 / 512) -> Problem:
+    """Thick elliptical shell of PAPER.md:1588-1634: r1 = 0.2, r2 = 0.25, thickness
+    gamma = 0.0625, N_s = 75N/16, N_r = 3N/8 circumferential fibres with stiffness
+    sigma(r) = 1 - cos 2 pi r, rest length 0; fibre j at r_j = (j + 1/2)/N_r, weights
+    h_s h_r (R22); fluid at rest, rho = 1, the paper's delta kernel."""
+    ns, nr = 75 * n // 16, 3 * n // 8
+    r1, r2, gam = 0.2, 0.25, 0.0625
+    s = np.arange(ns) / ns
+    Xs, Es, Ks = [], [], []
+    for jr in range(nr):
+        r = (jr + 0.5) / nr
+        Xs.append(np.stack([0.5 + (r1 + gam * (r - 0.5)) * np.cos(2 * np.pi * s),
+                            0.5 + (r2 + gam * (r - 0.5)) * np.sin(2 * np.pi * s)], 1))
+        k = np.arange(ns)
+        Es.append(np.stack([k, (k + 1) % ns], 1) + jr * ns)
+        Ks.append(np.full(ns, (1 - np.cos(2 * np.pi * r)) * ns ** 2))
+    pr = Problem(f"thick_shell_n{n}", 2, n, mu, 1.0, dt, 0, kernel=PESKIN4)
+    pr.u = [np.zeros((n, n)), np.zeros((n, n))]
+    pr.p = np.zeros((n, n))
+    pr.X = np.ascontiguousarray(np.concatenate(Xs))
+    pr.edges = np.ascontiguousarray(np.concatenate(Es).astype(np.int64))
+    pr.kappa = np.concatenate(Ks)
+    pr.weight = np.full(ns * nr, 1.0 / (ns * nr))
+    return pr
+
+
+def cylinder_shell(n: int, sigma_s: float = 1.0, sigma_r: float = 1.0, rest: float = 1.0,
+                   mu: float = 0.01) -> Problem:
+    """3D cylindrical shell of PAPER.md:2078-2118: X(s, r) = (r, 1/2 + r1 cos 2 pi s,
+    1/2 + r2 sin 2 pi s), r1 = 5/28, r2 = 7/20, N_s = 19N/4 fibres around (stiffness
+    sigma_s, rest length 0) interwoven with N_r = 3N axial fibres (stiffness sigma_r,
+    rest length L = 1), periodic in x (no cuts), dt = 0.04/N.  Force connections in the
+    form of PAPER.md:856-861: kappa = sigma/h^2 and rest length L h along each family,
+    quadrature weight h_s h_r (R26)."""
+    ns, nr = 19 * n // 4, 3 * n
+    hs, hr = 1.0 / ns, 1.0 / nr
+    r1, r2 = 5.0 / 28.0, 7.0 / 20.0
+    s = np.arange(ns) / ns
+    r = np.arange(nr) / nr
+    R, S = np.meshgrid(r, s, indexing="ij")            # point (jr, js) -> jr * ns + js
+    X = np.stack([R.ravel(), (0.5 + r1 * np.cos(2 * np.pi * S)).ravel(),
+                  (0.5 + r2 * np.sin(2 * np.pi * S)).ravel()], 1)
+    jr, js = np.meshgrid(np.arange(nr), np.arange(ns), indexing="ij")
+    idx = jr * ns + js
+    e_s = np.stack([idx.ravel(), (jr * ns + (js + 1) % ns).ravel()], 1)
+    e_r = np.stack([idx.ravel(), (((jr + 1) % nr) * ns + js).ravel()], 1)
+    pr = Problem(f"cylinder_n{n}", 3, n, mu, 1.0, 0.04 / n, 100, kernel=PESKIN4)
+    pr.u = [np.zeros((n, n, n)) for _ in range(3)]
+    pr.p = np.zeros((n, n, n))
+    pr.X = np.ascontiguousarray(X)
+    pr.edges = np.ascontiguousarray(np.concatenate([e_s, e_r]).astype(np.int64))
+    pr.kappa = np.concatenate([np.full(len(e_s), sigma_s / hs ** 2), np.full(len(e_r), sigma_r / hr ** 2)])
+    pr.rest = np.concatenate([np.zeros(len(e_s)), np.full(len(e_r), rest * hr)])
+    pr.weight = np.full(ns * nr, hs * hr)
+    return pr
+
+
 # ------------------------------------------------------------------ configs
 def config(idx: int, **over) -> Problem:
     """BASELINE.json configs[idx]; keyword overrides (n=, nodes=, pts=, steps=) give
