@@ -159,6 +159,17 @@ int ib_get_aux(ib_ctx* ctx, double* fu, double* fv, double* fw, double* nu, doub
  * Errors: IB_EINVAL (kappa < 0, axis >= dim, slab context and axis != dim-1). */
 int ib_line_solve(ib_ctx* ctx, int32_t axis, double kappa, const double* d, double* x);
 
+/* Stand-alone directional-split solve (eq. PoissonGMProblem with
+ * A = (1 - D_xx)(1 - D_yy)[(1 - D_zz)], D_aa = delta_aa / h^2, H = 1): copies the
+ * cell-centred right-hand side f (N^d doubles, host) to the device, applies A^{-1}
+ * `repeats` times in place (each application = one batched cyclic line pass per axis,
+ * the same kernels and mean correction as the psi factors of ib_step), and copies
+ * A^{-repeats} f to psi (host; may alias f).  *device_ms (may be NULL) receives the
+ * average device time of one application, measured with CUDA events on the context's
+ * stream around the line passes only.  Single-GPU contexts only.
+ * Errors: IB_EINVAL (repeats < 1, null f/psi, slab context). */
+int ib_psi_solve(ib_ctx* ctx, const double* f, double* psi, int32_t repeats, double* device_ms);
+
 /* Device-side finiteness check of u, p and X; IB_ENONFINITE if any NaN/Inf. */
 int ib_check_finite(ib_ctx* ctx);
 

@@ -353,7 +353,10 @@ void orc_op_spread(int dim, long n, int kernel, long npts, const double* X, cons
  * FC form of PAPER.md:856-861.  Edge e = (a, b) with stiffness kappa_e and rest length
  * L_e acts as  F_a += kappa_e (X_b - X_a)(1 - L_e/|X_b - X_a|),  F_b -= the same.
  * For a closed 2D fibre with kappa = sigma/h_s^2 and L_e = L h_s this is exactly
- * sigma D_s^-( D_s^+ X (1 - L/|D_s^+ X|) )  (R9/R10). */
+ * sigma D_s^-( D_s^+ X (1 - L/|D_s^+ X|) )  (R9/R10).
+ * X_b - X_a is the minimum-image displacement in the periodic unit box, so a fibre
+ * that closes through the boundary acts on its periodic copy ("the ends of the
+ * cylinder are connected to their periodic copies"; R26). */
 void orc_op_force(int dim, long npts, const double* X, long nedges, const int64_t* edges,
                   const double* kappa, const double* rest, double* F)
 {
@@ -361,7 +364,11 @@ void orc_op_force(int dim, long npts, const double* X, long nedges, const int64_
     for (long e = 0; e < nedges; e++) {
         long a = (long)edges[2 * e], b = (long)edges[2 * e + 1];
         double D[3] = {0, 0, 0}, len2 = 0.0;
-        for (int c = 0; c < dim; c++) { D[c] = X[b * dim + c] - X[a * dim + c]; len2 += D[c] * D[c]; }
+        for (int c = 0; c < dim; c++) {
+            D[c] = X[b * dim + c] - X[a * dim + c];
+            D[c] -= nearbyint(D[c]);          /* minimum image, box side 1 */
+            len2 += D[c] * D[c];
+        }
         double t = kappa[e];
         if (rest && rest[e] != 0.0) t = kappa[e] * (1.0 - rest[e] / sqrt(len2));
         for (int c = 0; c < dim; c++) { F[a * dim + c] += t * D[c]; F[b * dim + c] -= t * D[c]; }

@@ -1022,6 +1022,31 @@ int ib_line_solve(ib_ctx* c, int32_t axis, double kappa, const double* d, double
     return IB_OK;
 }
 
+int ib_psi_solve(ib_ctx* c, const double* f, double* psi, int32_t repeats, double* device_ms)
+{
+    if (!c || !f || !psi) return fail(IB_EINVAL, "null argument");
+    Ctx* s = &c->s;
+    if (repeats < 1) return fail(IB_EINVAL, "repeats must be >= 1");
+    if (s->grp) return fail(IB_EINVAL, "ib_psi_solve runs on a single-GPU context");
+    const size_t fb = (size_t)s->ncell * sizeof(double);
+    CKC(cudaMemcpyAsync(s->tmp, f, fb, cudaMemcpyHostToDevice, s->stream));
+    cudaEvent_t e0, e1;
+    CKC(cudaEventCreate(&e0));
+    CKC(cudaEventCreate(&e1));
+    CKC(cudaEventRecord(e0, s->stream));
+    for (int r = 0; r < repeats; ++r)
+        for (int a = s->dim - 1; a >= 0; --a) CKC(launch_line_solve(s, a, SYS_PSI, s->tmp));
+    CKC(cudaEventRecord(e1, s->stream));
+    CKC(cudaMemcpyAsync(psi, s->tmp, fb, cudaMemcpyDeviceToHost, s->stream));
+    CKC(cudaStreamSynchronize(s->stream));
+    float ms = 0.f;
+    CKC(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (device_ms) *device_ms = ms / repeats;
+    return IB_OK;
+}
+
 int ib_check_finite(ib_ctx* c)
 {
     if (!c) return fail(IB_EINVAL, "null context");

@@ -97,7 +97,9 @@ __global__ void k_interp_evolve(const double* __restrict__ u0, const double* __r
 
 // Step 2a: F_k = sum_{e=(k,m)} kappa_e (X_m - X_k)(1 - L_e/|X_m - X_k|) at X^{n+1/2}
 // (PAPER.md:607-614 in the force-connection form of PAPER.md:856-861), gathered per
-// point from a CSR adjacency (no atomics).
+// point from a CSR adjacency (no atomics).  X_m - X_k is the minimum-image displacement
+// in the periodic unit box (a fibre closing through the boundary connects to its
+// periodic copy; R26).
 template <int DIM>
 __global__ void k_force(const double* __restrict__ Xh, const int32_t* __restrict__ ptr,
                         const int32_t* __restrict__ nbr, const double* __restrict__ kap,
@@ -114,6 +116,7 @@ __global__ void k_force(const double* __restrict__ Xh, const int32_t* __restrict
 #pragma unroll
         for (int a = 0; a < DIM; ++a) {
             d[a] = Xh[(int64_t)m * DIM + a] - xk[a];
+            d[a] -= rint(d[a]);
             l2 += d[a] * d[a];
         }
         double t = kap[e];

@@ -42,7 +42,7 @@ _lib = None
 SYMBOLS = ["ib_default_options", "ib_create", "ib_set_fields", "ib_set_boundary", "ib_set_fibers",
            "ib_step", "ib_sync", "ib_get_fields", "ib_get_aux", "ib_line_solve", "ib_check_finite",
            "ib_get_stats", "ib_destroy", "ib_last_error", "ib_set_profiling", "ib_get_phase_times",
-           "ib_set_debug", "ib_nccl_unique_id", "ib_slab_range"]
+           "ib_set_debug", "ib_nccl_unique_id", "ib_slab_range", "ib_psi_solve"]
 
 PHASES = ["interp_evolve", "force", "spread", "s1_rhs_xsweep", "sweep_y", "sweep_z", "div_psi_first",
           "psi_y", "psi_x_p", "clear"]
@@ -83,6 +83,7 @@ def lib():
         L.ib_get_phase_times.argtypes = [ctypes.c_void_p, _dp, _i64p]
         L.ib_set_debug.argtypes = [ctypes.c_void_p, ctypes.c_int32]
         L.ib_nccl_unique_id.argtypes = [ctypes.c_void_p]
+        L.ib_psi_solve.argtypes = [ctypes.c_void_p, _dp, _dp, ctypes.c_int32, _dp]
         L.ib_slab_range.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, _i64p, _i64p]
         for name in SYMBOLS:
             if name not in ("ib_default_options", "ib_last_error"):
@@ -244,6 +245,15 @@ class Context:
         x = np.empty_like(d)
         _ck(lib().ib_line_solve(self._h, axis, kappa, _p(d), _p(x)))
         return x
+
+    def psi_solve(self, f, repeats=1):
+        """ib_psi_solve: A^{-repeats} f with A = prod_a (1 - D_aa); returns (psi, device ms
+        per application)."""
+        f = _c(f)
+        x = np.empty_like(f)
+        ms = ctypes.c_double()
+        _ck(lib().ib_psi_solve(self._h, _p(f), _p(x), int(repeats), ctypes.byref(ms)))
+        return x, ms.value
 
     def check_finite(self):
         _ck(lib().ib_check_finite(self._h))

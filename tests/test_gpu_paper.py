@@ -65,3 +65,38 @@ def test_table5_thick_shell_rates_mu005():
     ref = [G[("T5", f"mu=0.05,{q}")] for q in ("u", "p", "X")]
     assert abs(r[0] - ref[0]) <= 0.1 and abs(r[2] - ref[2]) <= 0.1, (r, ref)
     assert abs(r[1] - ref[1]) <= 0.15, (r, ref)
+
+
+@pytest.mark.parametrize("dim,n", [(2, 256), (2, 1024), (3, 64), (3, 128)])
+def test_ds_solve_closed_form(dim, n):
+    """§8(f2): A^{-1} f for the paper's single-mode f equals
+    f / (1 + lam)^d, lam = 4 sin^2(pi h)/h^2, the exact discrete solution."""
+    import bench_ds_solve as B
+    r = B.run(dim, n, 3)
+    assert r["rel_err"] <= 1e-12, r
+
+
+def test_cylinder_is_the_thin_ellipse_extruded():
+    """§8(f3): the 3D cylinder (axial fibres at their rest length
+    L = 1) starts x-invariant, so it must evolve as the 2D thin ellipse: cross-section
+    positions and the (v, w, p) slices equal the 2D (X, u, v, p) for every x, and
+    u_x stays at rounding level.  The x-sum of the delta weights over the axial points
+    (spacing h/3) is exactly 1, so the 3D force per unit length is the 2D force."""
+    from paper_1305_3976_b200 import ibgm, inputs
+    n, steps = 32, 40
+    c3 = inputs.cylinder_shell(n)
+    c2 = inputs.thin_ellipse(n, dt=c3.dt)
+    g3, g2 = ibgm.from_problem(c3), ibgm.from_problem(c2)
+    g3.step(steps); g2.step(steps)
+    f3, f2 = g3.fields(), g2.fields()
+    ns = 19 * n // 4
+    X3 = f3["X"].reshape(3 * n, ns, 3)
+    scale = np.abs(f2["u"][0]).max()
+    assert scale > 0
+    assert np.abs(X3[:, :, 1:] - f2["X"][None]).max() <= 1e-11
+    assert np.abs(f3["u"][0]).max() <= 1e-9 * scale
+    for i in range(n):
+        assert np.abs(f3["u"][1][:, :, i] - f2["u"][0]).max() <= 1e-9 * scale
+        assert np.abs(f3["u"][2][:, :, i] - f2["u"][1]).max() <= 1e-9 * scale
+        assert np.abs(f3["p"][:, :, i] - f2["p"]).max() <= 1e-9 * np.abs(f2["p"]).max()
+    g3.close(); g2.close()

@@ -502,3 +502,23 @@ def test_table6_divergence_error_thick_shell(oracle, row):
     dv = oracle.div(fo["u"][0], fo["u"][1])
     err = math.sqrt((dv ** 2).sum() / n ** 2)
     assert abs(err - ref) < 0.02 * ref, (err, ref)
+
+
+def test_force_minimum_image_through_the_boundary(oracle):
+    """R26 (fibres connected to their periodic copies): a spring
+    whose endpoints sit on opposite sides of the periodic boundary acts through the
+    boundary -- the same force as with the far endpoint moved to its nearby image --
+    and a straight periodic chain at rest length exerts no force."""
+    X = np.array([[0.05, 0.5], [0.95, 0.52]])
+    Xi = np.array([[0.05, 0.5], [-0.05, 0.52]])
+    E = np.array([[0, 1]], dtype=np.int64)
+    for rest in (None, np.array([0.03])):
+        F = oracle.force(X, E, np.array([7.0]), rest)
+        Fi = oracle.force(Xi, E, np.array([7.0]), rest)
+        assert np.abs(F - Fi).max() <= 1e-12 * np.abs(Fi).max()
+        assert Fi[0, 0] < 0   # pulled towards -x, through the boundary
+    n = 12
+    Xc = np.stack([np.arange(n) / n, np.full(n, 0.5)], 1)
+    Ec = np.stack([np.arange(n), (np.arange(n) + 1) % n], 1).astype(np.int64)
+    Fc = oracle.force(Xc, Ec, np.full(n, 3.0), np.full(n, 1.0 / n))
+    assert np.abs(Fc).max() <= 1e-12
