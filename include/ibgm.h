@@ -67,7 +67,9 @@ typedef struct {
     int32_t dim; /* 2 or 3 */
     int64_t n;   /* cells per side N; must have a divisor L in {2,3,4,6,8,12,16,24,32}
                     with N/L <= 32 (line-solve segmentation), 8 <= N <= 1024           */
-    double H;    /* box side; must be 1 (the psi operator (1 - D_aa) is literal, R2)  */
+    double H;    /* box side H > 0 (1 in every BASELINE config); h = H/N in every
+                    operator, including the literal psi operator (1 - D_aa),
+                    D_aa = delta_aa/h^2 (R2); positions live in [0, H)^d */
 } ib_grid;
 
 typedef struct {
@@ -97,7 +99,7 @@ void ib_default_options(ib_options* opt);
  * buffer and precomputes the line-solver factors.  *out receives the context.
  * With nranks > 1 and the NCCL transport every rank calls ib_create collectively
  * (ncclCommInitRank on device `device`).
- * Errors: IB_EINVAL (dim not 2/3, N unsupported, H != 1, dt <= 0, rho <= 0, nu < 0,
+ * Errors: IB_EINVAL (dim not 2/3, N unsupported, H <= 0, dt <= 0, rho <= 0, nu < 0,
  * chi not in (0,1], N % nranks != 0, N/nranks < 2, rank out of range, NCCL transport
  * without nccl_id), IB_ENCCL, IB_ECUDA, IB_ENOMEM. */
 int ib_create(const ib_grid* grid, double nu, double rho, double dt, const ib_options* opt,

@@ -35,13 +35,16 @@
 #define ORC_PESKIN4 1 /* PAPER.md:510-520, eq. (discretedelta)                           */
 
 /* ------------------------------------------------------------------------- */
-/* Grid helpers.  Periodic box [0,1]^d, N cells per side, h = 1/N            */
+/* Grid helpers.  Periodic box [0,H]^d, N cells per side, h = H/N (H = 1 in */
+/* every BASELINE config; the P x P ellipse array of PAPER.md:1972-2003 is    */
+/* H = P, R2)                                                       */
 /* (PAPER.md:413-446).  Storage: idx = i + N*(j + N*k), x fastest.           */
 /* ------------------------------------------------------------------------- */
 typedef struct {
     int dim;
     long n;
     double h;
+    double H;     /* box side */
 } orc_grid;
 
 static long wrap(long i, long n)
@@ -284,14 +287,14 @@ static void solve_axis(const orc_grid* g, double* q, int ax, double c, double a,
 /* Exported: solve every line of the N^dim array q along `axis`, in place. */
 void orc_solve_axis(int dim, long n, int axis, double c, double a, double b, double* q)
 {
-    orc_grid g = {dim, n, 1.0 / (double)n};
+    orc_grid g = {dim, n, 1.0 / (double)n, 1.0};
     solve_axis(&g, q, axis, c, a, b);
 }
 
 /* ------------------------------------------------------------------------- */
 /* Exported single-operator entry points (used by the oracle's pin tests).    */
 /* ------------------------------------------------------------------------- */
-static orc_grid mkgrid(int dim, long n) { orc_grid g = {dim, n, 1.0 / (double)n}; return g; }
+static orc_grid mkgrid(int dim, long n) { orc_grid g = {dim, n, 1.0 / (double)n, 1.0}; return g; }
 
 #define LOOP_CELLS(g)                                              \
     for (long k = 0; k < ((g).dim == 3 ? (g).n : 1); k++)          \
@@ -328,25 +331,37 @@ void orc_op_adv(int dim, long n, const double* u, const double* v, const double*
 }
 
 /* interpolate all components at npts points X[npts][dim] -> U[npts][dim] */
+static void interp_grid(const orc_grid* g, int kernel, const double* u, const double* v, const double* w,
+                        long npts, const double* X, double* U)
+{
+    const double* F[3] = {u, v, w};
+    for (long p = 0; p < npts; p++)
+        for (int c = 0; c < g->dim; c++) U[p * g->dim + c] = interp1(g, kernel, F[c], c, X + p * g->dim);
+}
+
 void orc_op_interp(int dim, long n, int kernel, const double* u, const double* v, const double* w,
                    long npts, const double* X, double* U)
 {
     orc_grid g = mkgrid(dim, n);
-    const double* F[3] = {u, v, w};
-    for (long p = 0; p < npts; p++)
-        for (int c = 0; c < dim; c++) U[p * dim + c] = interp1(&g, kernel, F[c], c, X + p * dim);
+    interp_grid(&g, kernel, u, v, w, npts, X, U);
 }
 
 /* spread forces F[npts][dim] with quadrature weights wgt[npts] (NULL -> 1) into
  * zeroed-or-not f arrays (accumulates) */
+static void spread_grid(const orc_grid* g, int kernel, long npts, const double* X, const double* F,
+                        const double* wgt, double* fu, double* fv, double* fw)
+{
+    double* O[3] = {fu, fv, fw};
+    for (long p = 0; p < npts; p++)
+        for (int c = 0; c < g->dim; c++)
+            spread1(g, kernel, O[c], c, X + p * g->dim, F[p * g->dim + c] * (wgt ? wgt[p] : 1.0));
+}
+
 void orc_op_spread(int dim, long n, int kernel, long npts, const double* X, const double* F,
                    const double* wgt, double* fu, double* fv, double* fw)
 {
     orc_grid g = mkgrid(dim, n);
-    double* O[3] = {fu, fv, fw};
-    for (long p = 0; p < npts; p++)
-        for (int c = 0; c < dim; c++)
-            spread1(&g, kernel, O[c], c, X + p * dim, F[p * dim + c] * (wgt ? wgt[p] : 1.0));
+    spread_grid(&g, kernel, npts, X, F, wgt, fu, fv, fw);
 }
 
 /* Elastic force of the force-connection network, Step 2a in the
@@ -357,8 +372,17 @@ void orc_op_spread(int dim, long n, int kernel, long npts, const double* X, cons
  * X_b - X_a is the minimum-image displacement in the periodic unit box, so a fibre
  * that closes through the boundary acts on its periodic copy ("the ends of the
  * cylinder are connected to their periodic copies"; R26). */
+static void force_box(int dim, long npts, const double* X, long nedges, const int64_t* edges,
+                      const double* kappa, const double* rest, double* F, double H);
+
 void orc_op_force(int dim, long npts, const double* X, long nedges, const int64_t* edges,
                   const double* kappa, const double* rest, double* F)
+{
+    force_box(dim, npts, X, nedges, edges, kappa, rest, F, 1.0);
+}
+
+static void force_box(int dim, long npts, const double* X, long nedges, const int64_t* edges,
+                      const double* kappa, const double* rest, double* F, double H)
 {
     for (long p = 0; p < npts * dim; p++) F[p] = 0.0;
     for (long e = 0; e < nedges; e++) {
@@ -366,7 +390,7 @@ void orc_op_force(int dim, long npts, const double* X, long nedges, const int64_
         double D[3] = {0, 0, 0}, len2 = 0.0;
         for (int c = 0; c < dim; c++) {
             D[c] = X[b * dim + c] - X[a * dim + c];
-            D[c] -= nearbyint(D[c]);          /* minimum image, box side 1 */
+            D[c] -= H * nearbyint(D[c] / H);  /* minimum image, box side H */
             len2 += D[c] * D[c];
         }
         double t = kappa[e];
@@ -394,12 +418,24 @@ typedef struct {
 
 void orc_destroy(orc_state* s);
 
+orc_state* orc_create_box(int dim, long n, double H, double mu, double rho, double dt, double chi,
+                          int kernel, int advection, int rotate);
+
 orc_state* orc_create(int dim, long n, double mu, double rho, double dt, double chi,
                       int kernel, int advection, int rotate)
 {
-    if ((dim != 2 && dim != 3) || n < 4) return NULL;
+    return orc_create_box(dim, n, 1.0, mu, rho, dt, chi, kernel, advection, rotate);
+}
+
+/* the box [0,H]^d: h = H/N in every operator (D_aa = delta_aa/h^2 literally, R2) */
+orc_state* orc_create_box(int dim, long n, double H, double mu, double rho, double dt, double chi,
+                          int kernel, int advection, int rotate)
+{
+    if ((dim != 2 && dim != 3) || n < 4 || !(H > 0)) return NULL;
     orc_state* s = (orc_state*)calloc(1, sizeof(orc_state));
     s->g = mkgrid(dim, n);
+    s->g.H = H;
+    s->g.h = H / (double)n;
     s->mu = mu; s->rho = rho; s->dt = dt; s->chi = chi;
     s->kernel = kernel; s->advection = advection; s->rotate = rotate;
     s->nc = ncell(&s->g);
@@ -477,7 +513,7 @@ static void one_step(orc_state* s)
     const double dt = s->dt, rho = s->rho, mu = s->mu;
 
     /* Step 1a: U^n = interpolate u^n at X^n */
-    orc_op_interp(d, g->n, s->kernel, s->u[0], s->u[1], d == 3 ? s->u[2] : NULL, s->npts, s->X, s->U);
+    interp_grid(g, s->kernel, s->u[0], s->u[1], d == 3 ? s->u[2] : NULL, s->npts, s->X, s->U);
 
     /* Step 1b: X^{n+1} = X^n + dt (3/2 U^n - 1/2 U^{n-1}); forward Euler at n = 0
      * */
@@ -489,11 +525,11 @@ static void one_step(orc_state* s)
     }
 
     /* Step 2a: F^{n+1/2} at X^{n+1/2} */
-    orc_op_force(d, s->npts, s->Xh, s->nedges, s->edges, s->kappa, s->rest, s->F);
+    force_box(d, s->npts, s->Xh, s->nedges, s->edges, s->kappa, s->rest, s->F, g->H);
 
     /* Step 2b: f^{n+1/2} = sum_k F_k delta_h(x - X^{n+1/2}_k) w_k */
     for (int c = 0; c < d; c++) memset(s->f[c], 0, sizeof(double) * nc);
-    orc_op_spread(d, g->n, s->kernel, s->npts, s->Xh, s->F, s->wgt, s->f[0], s->f[1], d == 3 ? s->f[2] : NULL);
+    spread_grid(g, s->kernel, s->npts, s->Xh, s->F, s->wgt, s->f[0], s->f[1], d == 3 ? s->f[2] : NULL);
 
     /* Step 3a: p* = p^{n-1/2} + psi^{n-1/2}; p* = 0 at n = 0 */
     /* (kept in s->r temporarily) */

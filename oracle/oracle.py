@@ -60,6 +60,10 @@ def lib():
         L.orc_create.argtypes = [ctypes.c_int, ctypes.c_long, ctypes.c_double, ctypes.c_double,
                                  ctypes.c_double, ctypes.c_double, ctypes.c_int, ctypes.c_int,
                                  ctypes.c_int]
+        L.orc_create_box.restype = ctypes.c_void_p
+        L.orc_create_box.argtypes = [ctypes.c_int, ctypes.c_long, ctypes.c_double, ctypes.c_double,
+                                     ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int,
+                                     ctypes.c_int, ctypes.c_int]
         L.orc_destroy.argtypes = [ctypes.c_void_p]
         L.orc_set_fields.argtypes = [ctypes.c_void_p, _dp, _dp, _dp, _dp]
         L.orc_set_boundary.restype = ctypes.c_int
@@ -177,9 +181,9 @@ class Oracle:
     """Plain CPU IB-GM stepper (the test oracle).  Field arrays are numpy
     [k][j][i] (3D) or [j][i] (2D), x fastest."""
 
-    def __init__(self, dim, n, mu, rho, dt, chi=0.6, kernel=COS4, advection=True, rotate=True):
+    def __init__(self, dim, n, mu, rho, dt, chi=0.6, kernel=COS4, advection=True, rotate=True, H=1.0):
         self.dim, self.n = dim, n
-        self._h = lib().orc_create(dim, n, mu, rho, dt, chi, kernel, int(advection), int(rotate))
+        self._h = lib().orc_create_box(dim, n, H, mu, rho, dt, chi, kernel, int(advection), int(rotate))
         if not self._h:
             raise MemoryError("orc_create failed")
         self.npts = 0

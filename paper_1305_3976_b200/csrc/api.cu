@@ -362,7 +362,7 @@ int ib_create(const ib_grid* grid, double nu, double rho, double dt, const ib_op
     if (opt) o = *opt; else ib_default_options(&o);
     if (grid->dim != 2 && grid->dim != 3) return fail(IB_EINVAL, "dim must be 2 or 3 (got %d)", grid->dim);
     if (grid->n < 8 || grid->n > 1024) return fail(IB_EINVAL, "N must be in [8, 1024] (got %lld)", (long long)grid->n);
-    if (grid->H != 1.0) return fail(IB_EINVAL, "H must be 1 (the psi operator is literal, DESIGN.md R2)");
+    if (!(grid->H > 0)) return fail(IB_EINVAL, "the box side H must be > 0");
     if (!(dt > 0) || !(rho > 0) || !(nu >= 0)) return fail(IB_EINVAL, "need dt > 0, rho > 0, nu >= 0");
     if (!(o.chi > 0 && o.chi <= 1)) return fail(IB_EINVAL, "chi must be in (0, 1]");
     if (o.kernel != IB_DELTA_COS4 && o.kernel != IB_DELTA_PESKIN4) return fail(IB_EINVAL, "unknown delta kernel");
@@ -393,7 +393,8 @@ int ib_create(const ib_grid* grid, double nu, double rho, double dt, const ib_op
     s->n = grid->n;
     s->ncell = grid->dim == 3 ? grid->n * grid->n * grid->n : grid->n * grid->n;
     s->plane = grid->dim == 3 ? grid->n * grid->n : grid->n;
-    s->h = 1.0 / (double)grid->n;
+    s->H = grid->H;
+    s->h = grid->H / (double)grid->n;       // every operator uses h = H/N (R2)
     s->rho = rho;
     s->mu = nu * rho;
     s->dt = dt;
@@ -449,7 +450,7 @@ int ib_create(const ib_grid* grid, double nu, double rho, double dt, const ib_op
             Ctx* sl = new Ctx();
             memset(sl, 0, sizeof(*sl));
             sl->dim = s->dim; sl->n = s->n; sl->ncell = s->ncell; sl->plane = s->plane;
-            sl->h = s->h; sl->mu = s->mu; sl->rho = s->rho; sl->dt = s->dt; sl->chi = s->chi;
+            sl->h = s->h; sl->H = s->H; sl->mu = s->mu; sl->rho = s->rho; sl->dt = s->dt; sl->chi = s->chi;
             sl->kernel = s->kernel; sl->advection = s->advection; sl->device = s->device;
             sl->stream = s->stream; sl->own_stream = false;
             sl->L = L; sl->P = Pseg;

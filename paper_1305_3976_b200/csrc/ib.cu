@@ -103,7 +103,8 @@ __global__ void k_interp_evolve(const double* __restrict__ u0, const double* __r
 template <int DIM>
 __global__ void k_force(const double* __restrict__ Xh, const int32_t* __restrict__ ptr,
                         const int32_t* __restrict__ nbr, const double* __restrict__ kap,
-                        const double* __restrict__ rest, int has_rest, double* __restrict__ F, int64_t npts)
+                        const double* __restrict__ rest, int has_rest, double* __restrict__ F, int64_t npts,
+                        double H, double invH)
 {
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k >= npts) return;
@@ -116,7 +117,7 @@ __global__ void k_force(const double* __restrict__ Xh, const int32_t* __restrict
 #pragma unroll
         for (int a = 0; a < DIM; ++a) {
             d[a] = Xh[(int64_t)m * DIM + a] - xk[a];
-            d[a] -= rint(d[a]);
+            d[a] -= H * rint(d[a] * invH);
             l2 += d[a] * d[a];
         }
         double t = kap[e];
@@ -968,10 +969,12 @@ cudaError_t launch_force(Ctx* s)
     const int thr = 128;
     if (s->dim == 2)
         k_force<2><<<nblk(s->npts, thr), thr, 0, s->stream>>>(s->Xh, s->csr_ptr, s->csr_nbr, s->csr_kappa,
-                                                              s->csr_rest, s->has_rest, s->F, s->npts);
+                                                              s->csr_rest, s->has_rest, s->F, s->npts, s->H,
+                                                              1.0 / s->H);
     else
         k_force<3><<<nblk(s->npts, thr), thr, 0, s->stream>>>(s->Xh, s->csr_ptr, s->csr_nbr, s->csr_kappa,
-                                                              s->csr_rest, s->has_rest, s->F, s->npts);
+                                                              s->csr_rest, s->has_rest, s->F, s->npts, s->H,
+                                                              1.0 / s->H);
     s->launches++;
     return cudaGetLastError();
 }

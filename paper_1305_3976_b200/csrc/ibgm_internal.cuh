@@ -52,7 +52,7 @@ struct Ctx {
     int64_t nl, z0, plane, nlocal, hoff;
     int wrap, rank;
     Group* grp;                       // z-slab decomposition (nullptr on a single GPU)
-    double h, mu, rho, dt, chi;
+    double h, H, mu, rho, dt, chi;   // h = H/N, H the box side
     int kernel, advection, device;
     cudaStream_t stream;
     bool own_stream;

@@ -140,13 +140,13 @@ class Context:
     global)."""
 
     def __init__(self, dim, n, nu, rho, dt, *, kernel=IB_DELTA_COS4, chi=0.6, advection=True, device=0,
-                 stream=None, nranks=1, rank=0, transport=IB_TRANSPORT_NCCL, nccl_id=None):
+                 stream=None, nranks=1, rank=0, transport=IB_TRANSPORT_NCCL, nccl_id=None, H=1.0):
         L = lib()
         self.dim, self.n = dim, n
         self.nranks, self.rank, self.transport = nranks, rank, transport
         self.local = nranks > 1 and transport == IB_TRANSPORT_NCCL   # fields are this rank's slab
         self.nz = n // nranks if self.local else n
-        g = ib_grid(dim, n, 1.0)
+        g = ib_grid(dim, n, float(H))
         o = ib_options()
         L.ib_default_options(ctypes.byref(o))
         o.kernel, o.chi, o.advection, o.device = kernel, chi, int(advection), device
@@ -288,7 +288,7 @@ def slab_of(a, nranks, rank):
 def from_problem(pr, **kw):
     """Context + state from an inputs.Problem (fields cut to the local slab when the
     context holds one)."""
-    ctx = Context(pr.dim, pr.n, pr.mu / pr.rho, pr.rho, pr.dt, kernel=pr.kernel, chi=pr.chi, **kw)
+    ctx = Context(pr.dim, pr.n, pr.mu / pr.rho, pr.rho, pr.dt, kernel=pr.kernel, chi=pr.chi, H=pr.H, **kw)
     cut = (lambda a: a if a is None or not ctx.local else slab_of(a, ctx.nranks, ctx.rank))
     u = [cut(x) for x in pr.u]
     p = cut(pr.p)

@@ -32,6 +32,7 @@ class Problem:
     steps: int
     kernel: int = COS4
     chi: float = 0.6
+    H: float = 1.0                # box side (h = H/N)
     u: List[np.ndarray] = field(default_factory=list)     # dim arrays
     p: Optional[np.ndarray] = None
     X: np.ndarray = None          # [npts][dim]
@@ -226,6 +227,24 @@ def cylinder_shell(n: int, sigma_s: float = 1.0, sigma_r: float = 1.0, rest: flo
     pr.kappa = np.concatenate([np.full(len(e_s), sigma_s / hs ** 2), np.full(len(e_r), sigma_r / hr ** 2)])
     pr.rest = np.concatenate([np.zeros(len(e_s)), np.full(len(e_r), rest * hr)])
     pr.weight = np.full(ns * nr, hs * hr)
+    return pr
+
+
+def ellipse_array(P: int, n_cell: int = 128, sigma: float = 1.0, t_background=(0.5, 0.5 * np.sqrt(3.0)),
+                  dt_over_h: float = 0.01, mu: float = 0.01) -> Problem:
+    """P x P array of thin ellipses of PAPER.md:1972-2003 on the box [0, P]^2 (H = P,
+    N = P n_cell, h = 1/n_cell): ellipse (l, m) centred in its unit cell, r1 = 5/28,
+    r2 = 7/20, h_s = 4h/19 (N_s = 19 n_cell/4 points), sigma = 1, constant background
+    velocity u(x, 0) = (1, sqrt 3)/2, dt = 0.01 h, the paper's delta kernel."""
+    n = P * n_cell
+    h = 1.0 / n_cell
+    ns = 19 * n_cell // 4
+    pr = Problem(f"ellipse_array_{P}x{P}_n{n_cell}", 2, n, mu, 1.0, dt_over_h * h, 0, kernel=PESKIN4, H=float(P))
+    pr.u = [np.full((n, n), float(t_background[0])), np.full((n, n), float(t_background[1]))]
+    pr.p = np.zeros((n, n))
+    parts = [ellipse_fibre(ns, (l + 0.5, m + 0.5), (5.0 / 28.0, 7.0 / 20.0), sigma)
+             for m in range(P) for l in range(P)]
+    pr.X, pr.edges, pr.kappa, pr.weight = _concat(parts)
     return pr
 
 

@@ -100,3 +100,26 @@ def test_cylinder_is_the_thin_ellipse_extruded():
         assert np.abs(f3["u"][2][:, :, i] - f2["u"][1]).max() <= 1e-9 * scale
         assert np.abs(f3["p"][:, :, i] - f2["p"]).max() <= 1e-9 * np.abs(f2["p"]).max()
     g3.close(); g2.close()
+
+
+def test_ellipse_array_is_the_tiled_single_ellipse():
+    """§8(f4): on the doubly periodic box the P x P array of identical ellipses
+    (box [0,P]^2 at the same h) has the single-ellipse solution,
+    repeated ("a solution that is identical to that for a single membrane"): 40 steps
+    of the 2 x 2 array equal the 1 x 1 problem tiled, to rounding."""
+    from paper_1305_3976_b200 import ibgm, inputs
+    a = inputs.ellipse_array(2, n_cell=32, dt_over_h=0.01)
+    s1 = inputs.ellipse_array(1, n_cell=32, dt_over_h=0.01)
+    ga, gs = ibgm.from_problem(a), ibgm.from_problem(s1)
+    ga.step(40); gs.step(40)
+    fa, fs = ga.fields(), gs.fields()
+    for c in range(2):
+        ref = np.tile(fs["u"][c], (2, 2))
+        assert np.abs(fa["u"][c] - ref).max() <= 1e-10 * np.abs(ref).max()
+    refp = np.tile(fs["p"], (2, 2))
+    assert np.abs(fa["p"] - refp).max() <= 1e-10 * np.abs(refp).max()
+    ns = fs["X"].shape[0]
+    for b, (l, m) in enumerate([(0, 0), (1, 0), (0, 1), (1, 1)]):
+        Xb = fa["X"][b * ns:(b + 1) * ns] - np.array([l, m])
+        assert np.abs(Xb - fs["X"]).max() <= 1e-11
+    ga.close(); gs.close()

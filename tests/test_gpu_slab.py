@@ -25,7 +25,7 @@ def _rel(a, b):
 
 def _oracle_for(pr):
     from oracle import oracle as O
-    o = O.Oracle(pr.dim, pr.n, pr.mu, pr.rho, pr.dt, chi=pr.chi, kernel=pr.kernel)
+    o = O.Oracle(pr.dim, pr.n, pr.mu, pr.rho, pr.dt, chi=pr.chi, kernel=pr.kernel, H=pr.H)
     o.set_fields(*pr.u, p=pr.p) if pr.dim == 3 else o.set_fields(pr.u[0], pr.u[1], None, pr.p)
     if pr.X is not None:
         o.set_boundary(pr.X, pr.edges, pr.kappa, rest=pr.rest, weight=pr.weight)
@@ -186,4 +186,24 @@ def test_one_slab_transports(transport):
     x = g.line_solve(2, 32.0 ** 2, d)
     from oracle import oracle as O
     assert _rel(x, O.solve_axis(d, 2, -1024.0, 2049.0, -1024.0)) <= 1e-12
+    g.close(); g1.close()
+
+
+def test_ellipse_array_points_cross_slabs():
+    """§8(f4): the 2 x 2 ellipse array of PAPER.md:1972-2003 (box [0,2]^2, background
+    velocity (1, sqrt 3)/2) on 4 y-slabs: the membranes drift across slab boundaries
+    (replicated Lagrangian data, owner-only spreading, partial interpolation); 30
+    steps against the oracle and the single-GPU path."""
+    from paper_1305_3976_b200 import inputs
+    pr = inputs.ellipse_array(2, n_cell=32, dt_over_h=0.01)
+    o = _oracle_for(pr)
+    g = _gpu(pr, 4)
+    g1 = _gpu(pr, 1)
+    o.step(30); g.step(30); g1.step(30)
+    fo, fg, f1 = o.fields(), g.fields(), g1.fields()
+    for c in range(2):
+        assert _rel(fg["u"][c], fo["u"][c]) <= 1e-9 and _rel(fg["u"][c], f1["u"][c]) <= 1e-10
+    assert _rel(fg["p"], fo["p"]) <= 1e-9 and _rel(fg["X"], fo["X"]) <= 1e-9
+    # the background flow carried the membranes by ~30 dt |u| = 0.3 h
+    assert np.abs(fg["X"] - pr.X).max() > 0.1 / 32
     g.close(); g1.close()

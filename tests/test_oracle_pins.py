@@ -522,3 +522,22 @@ def test_force_minimum_image_through_the_boundary(oracle):
     Ec = np.stack([np.arange(n), (np.arange(n) + 1) % n], 1).astype(np.int64)
     Fc = oracle.force(Xc, Ec, np.full(n, 3.0), np.full(n, 1.0 / n))
     assert np.abs(Fc).max() <= 1e-12
+
+
+def test_box_side_H_array_equals_tiled_single(oracle):
+    """R2 for H != 1: on the box [0,2]^2 at the same h, the 2 x 2
+    array of identical ellipses (background flow (1, sqrt 3)/2) has exactly the tiled
+    single-ellipse solution -- which holds only if every operator uses h = H/N."""
+    from paper_1305_3976_b200 import inputs
+    res = []
+    for P in (2, 1):
+        pr = inputs.ellipse_array(P, n_cell=16, dt_over_h=0.01)
+        o = oracle.Oracle(2, pr.n, pr.mu, pr.rho, pr.dt, chi=pr.chi, kernel=pr.kernel, H=pr.H)
+        o.set_fields(pr.u[0], pr.u[1], None, pr.p)
+        o.set_boundary(pr.X, pr.edges, pr.kappa, weight=pr.weight)
+        o.step(5)
+        res.append(o.fields())
+    a, s = res
+    for c in range(2):
+        assert np.abs(a["u"][c] - np.tile(s["u"][c], (2, 2))).max() <= 1e-12 * np.abs(s["u"][c]).max()
+    assert np.abs(a["p"] - np.tile(s["p"], (2, 2))).max() <= 1e-12 * np.abs(s["p"]).max()
