@@ -1034,9 +1034,26 @@ int ib_psi_solve(ib_ctx* c, const double* f, double* psi, int32_t repeats, doubl
     cudaEvent_t e0, e1;
     CKC(cudaEventCreate(&e0));
     CKC(cudaEventCreate(&e1));
-    CKC(cudaEventRecord(e0, s->stream));
+    // the applications are captured once into a CUDA graph so that the device time is
+    // not bounded by host launch latency on small grids
+    for (int a = s->dim - 1; a >= 0; --a) CKC(launch_line_solve(s, a, SYS_PSI, s->tmp));   // first use: attributes
+    CKC(cudaMemcpyAsync(s->tmp, f, fb, cudaMemcpyHostToDevice, s->stream));
+    cudaGraph_t g;
+    cudaGraphExec_t ge;
+    CKC(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal));
     for (int r = 0; r < repeats; ++r)
-        for (int a = s->dim - 1; a >= 0; --a) CKC(launch_line_solve(s, a, SYS_PSI, s->tmp));
+        for (int a = s->dim - 1; a >= 0; --a) {
+            const cudaError_t le = launch_line_solve(s, a, SYS_PSI, s->tmp);
+            if (le != cudaSuccess) {
+                cudaStreamEndCapture(s->stream, &g);
+                return fail(IB_ECUDA, "launch_line_solve: %s", cudaGetErrorString(le));
+            }
+        }
+    CKC(cudaStreamEndCapture(s->stream, &g));
+    CKC(cudaGraphInstantiate(&ge, g, 0));
+    cudaGraphDestroy(g);
+    CKC(cudaEventRecord(e0, s->stream));
+    CKC(cudaGraphLaunch(ge, s->stream));
     CKC(cudaEventRecord(e1, s->stream));
     CKC(cudaMemcpyAsync(psi, s->tmp, fb, cudaMemcpyDeviceToHost, s->stream));
     CKC(cudaStreamSynchronize(s->stream));
@@ -1044,6 +1061,7 @@ int ib_psi_solve(ib_ctx* c, const double* f, double* psi, int32_t repeats, doubl
     CKC(cudaEventElapsedTime(&ms, e0, e1));
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    cudaGraphExecDestroy(ge);
     if (device_ms) *device_ms = ms / repeats;
     return IB_OK;
 }
