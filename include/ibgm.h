@@ -146,7 +146,10 @@ int ib_get_fields(ib_ctx* ctx, double* u, double* v, double* w, double* p, doubl
  * f^{n+1/2} per component (N^d each; requires ib_set_debug bit 0 before the step,
  * else IB_ESTATE), the stored advection N(u^n) per component,
  * the Lagrangian force F^{n+1/2} and X^{n+1/2} ([npts][dim]).  F is the force of
- * Step 2a BEFORE the quadrature weight is applied. */
+ * Step 2a BEFORE the quadrature weight is applied.  Without ib_set_debug bit 0 the
+ * single-GPU path runs the IB phase (Steps 1-2) of step n+1 concurrently with the psi
+ * passes of step n, so F, X^{n+1/2} and the history then already belong to the next
+ * step; set bit 0 (before stepping) to inspect the intermediates of each step. */
 int ib_get_aux(ib_ctx* ctx, double* fu, double* fv, double* fw, double* nu, double* nv,
                double* nw, double* F, double* Xh);
 

@@ -201,7 +201,7 @@ static bool choose_segmentation(int64_t n, int* L, int* P)
 
 static void drop_graphs(Ctx* s)
 {
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < 4; ++k) {
         if (s->gvalid[k]) cudaGraphExecDestroy(s->gexec[k]);
         s->gvalid[k] = false;
     }
@@ -213,6 +213,9 @@ static void free_lagrangian(Ctx* s)
     cudaFree(s->csr_ptr); cudaFree(s->csr_nbr); cudaFree(s->csr_kappa); cudaFree(s->csr_rest);
     cudaFree(s->bin_bid); cudaFree(s->bin_sorted);
     cudaFree(s->pt_user); cudaFree(s->lag_tmp);
+    cudaFree(s->Xold); cudaFree(s->Uold);
+    s->Xold = s->Uold = nullptr;
+    s->ib_ahead = false;
     s->pt_user = nullptr;
     s->lag_tmp = nullptr;
     s->bin_bid = s->bin_sorted = nullptr;
@@ -432,6 +435,14 @@ int ib_create(const ib_grid* grid, double nu, double rho, double dt, const ib_op
         s->nlocal = s->ncell;
         s->hoff = 0;
         CKC(alloc_fields(s));
+        // the look-ahead IB kernels (latency-bound, few blocks) get the higher priority so
+        // that their blocks take SM slots as the psi passes' blocks retire
+        int prio_lo = 0, prio_hi = 0;
+        CKC(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+        CKC(cudaStreamCreateWithPriority(&s->side, cudaStreamNonBlocking, prio_hi));
+        CKC(cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming));
+        CKC(cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming));
+        s->lookahead = 1;
     } else {
         // z-slab decomposition: the top context keeps the Lagrangian state; each slab
         // context holds the fields of nz planes (+ halos) and borrows the stream and the
@@ -520,6 +531,7 @@ int ib_set_fields(ib_ctx* c, const double* u, const double* v, const double* w, 
     }
     CKC(cudaStreamSynchronize(s->stream));
     s->step = 0;
+    s->ib_ahead = false;
     s->fields_set = true;
     return IB_OK;
 }
@@ -595,6 +607,9 @@ int ib_set_boundary(ib_ctx* c, int64_t npts, const double* X, int64_t nedges, co
     CKC(cudaMalloc(&s->csr_nbr, ne2 * sizeof(int32_t)));
     CKC(cudaMalloc(&s->csr_kappa, ne2 * sizeof(double)));
     CKC(cudaMalloc(&s->csr_rest, ne2 * sizeof(double)));
+    CKC(cudaMalloc(&s->Xold, pb));
+    CKC(cudaMalloc(&s->Uold, pb));
+    CKC(cudaMemsetAsync(s->Uold, 0, pb, s->stream));
     CKC(cudaMalloc(&s->pt_user, npts * sizeof(int32_t)));
     CKC(cudaMalloc(&s->lag_tmp, pb));
     CKC(cudaMemcpyAsync(s->pt_user, ord.data(), npts * sizeof(int32_t), cudaMemcpyHostToDevice, s->stream));
@@ -711,6 +726,20 @@ static void swap_state(Ctx* s)
 
 static int enqueue_any(Ctx* s, int first) { return s->grp ? enqueue_step_slab(s, first) : enqueue_step(s, first); }
 
+static bool lookahead_on(const Ctx* s)
+{
+    return s->lookahead && !s->grp && s->npts > 0 && !s->profiling && !s->debug_keep_f;
+}
+
+// Steps 1-2 (interpolate + evolve, force, spread) on context view v
+static cudaError_t enqueue_ib(Ctx* v, int first)
+{
+    cudaError_t e = launch_interp_evolve(v, first);
+    if (e == cudaSuccess) e = launch_force(v);
+    if (e == cudaSuccess) e = launch_spread(v);
+    return e;
+}
+
 int ib_step(ib_ctx* c, int64_t nsteps)
 {
     if (!c) return fail(IB_EINVAL, "null context");
@@ -720,8 +749,9 @@ int ib_step(ib_ctx* c, int64_t nsteps)
     for (int64_t t = 0; t < nsteps; ++t) {
         const int first = (s->step == 0);
         if (!first && !s->profiling && s->use_graphs && !s->debug_keep_f) {
-            // replay the captured regular step for the current pointer parity
-            const int par = s->parity;
+            // replay the captured regular step for the current pointer parity and
+            // look-ahead state
+            const int par = s->parity * 2 + (s->ib_ahead ? 1 : 0);
             if (!s->gvalid[par]) {
                 cudaGraph_t g;
                 const int64_t l0 = total_launches(s);
@@ -738,6 +768,7 @@ int ib_step(ib_ctx* c, int64_t nsteps)
             }
             CKC(cudaGraphLaunch(s->gexec[par], s->stream));
             s->launches += s->glaunches[par];
+            s->ib_ahead = lookahead_on(s);   // what the captured step leaves behind
         } else {
             const int rc = enqueue_any(s, first);
             if (rc != IB_OK) return rc;
@@ -767,7 +798,7 @@ static int enqueue_step(Ctx* s, int first)
         // n = 0: no N(u^{-1}); the history G starts as 0 + (2/rho) f
         if (first) PHASE(IB_PH_CLEAR, clear3(s, s->nprev));
         if (s->debug_keep_f && s->npts > 0) PHASE(IB_PH_CLEAR, clear3(s, s->f));
-        if (s->npts > 0) {
+        if (s->npts > 0 && !s->ib_ahead) {
             // Step 1 (interpolate, evolve) and Step 2 (force, spread)
             PHASE(IB_PH_INTERP, launch_interp_evolve(s, first));
             PHASE(IB_PH_FORCE, launch_force(s));
@@ -782,10 +813,27 @@ static int enqueue_step(Ctx* s, int first)
         } else {
             PHASE(IB_PH_SWEEP_Y, launch_sweep_last(s, 1));
         }
+        // look-ahead: Steps 1-2 of step n+1 need only u^{n+1} (now in st), X and U^n;
+        // they spread into N(u^n) (nadv, the next step's history G) while the psi passes
+        // below run on the main stream
+        const bool look = lookahead_on(s);
+        if (look) {
+            Ctx v = *s;
+            for (int q = 0; q < 3; ++q) { v.u[q] = s->st[q]; v.nprev[q] = s->nadv[q]; }
+            v.stream = s->side;
+            v.launches = 0;
+            CKC(cudaEventRecord(s->ev_fork, s->stream));
+            CKC(cudaStreamWaitEvent(s->side, s->ev_fork, 0));
+            CKC(enqueue_ib(&v, 0));
+            CKC(cudaEventRecord(s->ev_join, s->side));
+            s->launches += v.launches;
+        }
         // Step 3e: RHS and the psi factors (last axis first); Step 3f fused
         PHASE(IB_PH_DIVPSI, launch_div_psi_first(s, d - 1));
         if (d == 3) PHASE(IB_PH_PSI_Y, launch_psi_mid(s, 1));
         PHASE(IB_PH_PSI_X, launch_psi_last_x(s));
+        if (look) CKC(cudaStreamWaitEvent(s->stream, s->ev_join, 0));
+        s->ib_ahead = look;
     }
     return IB_OK;
 }
@@ -955,8 +1003,9 @@ int ib_get_fields(ib_ctx* c, double* u, double* v, double* w, double* p, double*
             CKC(cudaMemcpyAsync(psi + off, sl->tmp, fb, cudaMemcpyDeviceToHost, s->stream));
         }
     }
-    CKC(points_out(s, s->X, X));
-    CKC(points_out(s, s->Uprev, U));
+    // with the next step's IB phase already done, X^n and U^{n-1} are in Xold/Uold
+    CKC(points_out(s, s->ib_ahead ? s->Xold : s->X, X));
+    CKC(points_out(s, s->ib_ahead ? s->Uold : s->Uprev, U));
     CKC(cudaStreamSynchronize(s->stream));
     return IB_OK;
 }
@@ -1122,6 +1171,9 @@ int ib_destroy(ib_ctx* c)
     cudaFree(s->bin_nlist); cudaFree(s->bin_partial);
     if (s->ev_made)
         for (int ph = 0; ph < IB_NPHASES; ++ph) { cudaEventDestroy(s->ev[ph][0]); cudaEventDestroy(s->ev[ph][1]); }
+    if (s->side) cudaStreamDestroy(s->side);
+    if (s->ev_fork) cudaEventDestroy(s->ev_fork);
+    if (s->ev_join) cudaEventDestroy(s->ev_join);
     if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
     delete c;
     return IB_OK;

@@ -502,6 +502,9 @@ static int pick_r(const Ctx* s, int L, int nc)
     return 8;
 }
 
+template <int L, int KIND, int DIM, int AX, int NC, int MINB>
+static cudaError_t go_lines_k(Ctx* s, int sys, const LArgs& la, int ncomp_grid, int64_t rows, int gy);
+
 template <int L, int KIND, int DIM, int AX, int NC>
 static cudaError_t go_lines(Ctx* s, int sys, const LArgs& a, int ncomp_grid)
 {
@@ -512,7 +515,12 @@ static cudaError_t go_lines(Ctx* s, int sys, const LArgs& a, int ncomp_grid)
     la.wrap = s->wrap;
     const int64_t rows = (AX == 0 && DIM == 2) ? s->nl : s->n;
     const int gy = (DIM == 3) ? (int)s->nl : 1;
-    constexpr int MINB = (KIND == K_S1 || L >= 24) ? 2 : 4;
+    return go_lines_k<L, KIND, DIM, AX, NC, (KIND == K_S1 || L >= 24) ? 2 : 4>(s, sys, la, ncomp_grid, rows, gy);
+}
+
+template <int L, int KIND, int DIM, int AX, int NC, int MINB>
+static cudaError_t go_lines_k(Ctx* s, int sys, const LArgs& la, int ncomp_grid, int64_t rows, int gy)
+{
     auto kern = k_lines<L, KIND, DIM, AX, NC, MINB>;
     const int R = pick_r(s, L, tiles_of(KIND, NC));
     const size_t sm = lines_smem(s->P, L, tiles_of(KIND, NC), R);

@@ -45,8 +45,8 @@ __device__ __forceinline__ int wrap1(int i, int n) { return i >= n ? i - n : i; 
 template <int DIM, int KER>
 __global__ void k_interp_evolve(const double* __restrict__ u0, const double* __restrict__ u1,
                                 const double* __restrict__ u2, double* __restrict__ X, double* __restrict__ Xh,
-                                double* __restrict__ Uprev, int64_t npts, int n,
-                                double invh, double dt, int first)
+                                double* __restrict__ Uprev, double* __restrict__ Xold, double* __restrict__ Uold,
+                                int64_t npts, int n, double invh, double dt, int first)
 {
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k >= npts) return;
@@ -92,6 +92,8 @@ __global__ void k_interp_evolve(const double* __restrict__ u0, const double* __r
         Xh[k * DIM + c] = 0.5 * (xn + Xk[c]);
         X[k * DIM + c] = xn;
         Uprev[k * DIM + c] = acc;   // U^n becomes U^{n-1} of the next step
+        Xold[k * DIM + c] = Xk[c];  // X^n, U^{n-1}: the state before this step's IB phase
+        Uold[k * DIM + c] = up;
     }
 }
 
@@ -529,6 +531,7 @@ template <int DIM, int KER>
 __global__ void __launch_bounds__(kBoxPts * DIM) k_interp_box(const double* __restrict__ u0, const double* __restrict__ u1,
                                                             const double* __restrict__ u2, double* __restrict__ X,
                                                             double* __restrict__ Xh, double* __restrict__ Uprev,
+                                                            double* __restrict__ Xold, double* __restrict__ Uold,
                                                             int64_t npts, int n, double invh, double dt, int first)
 {
     extern __shared__ double box[];
@@ -618,6 +621,8 @@ __global__ void __launch_bounds__(kBoxPts * DIM) k_interp_box(const double* __re
     Xh[k * DIM + c] = 0.5 * (xn + xc);
     X[k * DIM + c] = xn;
     Uprev[k * DIM + c] = acc;
+    Xold[k * DIM + c] = xc;
+    Uold[k * DIM + c] = up;
 }
 
 // shared layout of the spread: box [DIM][VOL], then per (component, point) the weights
@@ -771,6 +776,7 @@ template <int DIM, int KER>
 __global__ void __launch_bounds__(256) k_interp_quad(const double* __restrict__ u0, const double* __restrict__ u1,
                                                      const double* __restrict__ u2, double* __restrict__ X,
                                                      double* __restrict__ Xh, double* __restrict__ Uprev,
+                                                     double* __restrict__ Xold, double* __restrict__ Uold,
                                                      int64_t npts, int n, double invh, double dt, int first)
 {
     const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 2;   // (component, point) group
@@ -826,6 +832,8 @@ __global__ void __launch_bounds__(256) k_interp_quad(const double* __restrict__ 
     Xh[k * DIM + c] = 0.5 * (xn + xc);
     X[k * DIM + c] = xn;
     Uprev[k * DIM + c] = acc;
+    Xold[k * DIM + c] = xc;
+    Uold[k * DIM + c] = up;
 }
 
 template <int DIM, int KER, bool KEEP>
@@ -928,7 +936,8 @@ cudaError_t launch_interp_evolve(Ctx* s, int first)
         const unsigned nbk = (unsigned)((thr + 255) / 256);
         const double invh = 1.0 / s->h;
 #define IBGM_IQ(D, K) k_interp_quad<D, K><<<nbk, 256, 0, s->stream>>>(s->u[0], s->u[1], s->u[2], s->X, s->Xh, \
-                                                                      s->Uprev, s->npts, (int)s->n, invh, s->dt, first)
+                                                                      s->Uprev, s->Xold, s->Uold, s->npts, (int)s->n, invh, \
+                                                                      s->dt, first)
         if (s->dim == 2) { if (s->kernel == IB_DELTA_COS4) IBGM_IQ(2, 0); else IBGM_IQ(2, 1); }
         else { if (s->kernel == IB_DELTA_COS4) IBGM_IQ(3, 0); else IBGM_IQ(3, 1); }
 #undef IBGM_IQ
@@ -944,7 +953,7 @@ cudaError_t launch_interp_evolve(Ctx* s, int first)
         const cudaError_t ae_ = box_attr<10 * D + K>(k_interp_box<D, K>, sm);                                         \
         if (ae_ != cudaSuccess) return ae_;                                                             \
         k_interp_box<D, K><<<nbk, kBoxPts * D, sm, s->stream>>>(s->u[0], s->u[1], s->u[2], s->X, s->Xh, \
-                                                                    s->Uprev, s->npts, (int)s->n, invh, s->dt, first); \
+                                                                    s->Uprev, s->Xold, s->Uold, s->npts, (int)s->n, invh, s->dt, first); \
     } while (0)
         if (s->dim == 2) { if (s->kernel == IB_DELTA_COS4) IBGM_IB(2, 0); else IBGM_IB(2, 1); }
         else { if (s->kernel == IB_DELTA_COS4) IBGM_IB(3, 0); else IBGM_IB(3, 1); }
@@ -955,7 +964,7 @@ cudaError_t launch_interp_evolve(Ctx* s, int first)
     const int thr = 128;
     const double invh = 1.0 / s->h;
 #define IBGM_IE(D, K) k_interp_evolve<D, K><<<nblk(s->npts, thr), thr, 0, s->stream>>>( \
-        s->u[0], s->u[1], s->u[2], s->X, s->Xh, s->Uprev, s->npts, (int)s->n, invh, s->dt, first)
+        s->u[0], s->u[1], s->u[2], s->X, s->Xh, s->Uprev, s->Xold, s->Uold, s->npts, (int)s->n, invh, s->dt, first)
     if (s->dim == 2) { if (s->kernel == IB_DELTA_COS4) IBGM_IE(2, 0); else IBGM_IE(2, 1); }
     else { if (s->kernel == IB_DELTA_COS4) IBGM_IE(3, 0); else IBGM_IE(3, 1); }
 #undef IBGM_IE

@@ -71,6 +71,7 @@ struct Ctx {
     // Lagrangian state (device)
     int64_t npts, nedges;
     double *X, *Xh, *Uprev, *F, *wgt;   // Uprev: U interpolated in the last step
+    double *Xold, *Uold;              // X and Uprev before the last IB phase (see ib_ahead)
     int32_t* csr_ptr;                 // [npts+1]
     int32_t* csr_nbr;                 // [2*nedges]
     double* csr_kappa;                // [2*nedges]
@@ -90,12 +91,20 @@ struct Ctx {
     bool fields_set;
     int64_t launches;
     int* d_flag;                      // device flag for finiteness checks
-    // CUDA graphs of one regular step, one per pointer parity (u <-> st, N <-> G swaps)
+    // IB look-ahead: the IB phase of step n+1 (Steps 1-2, which need only u^{n+1} and X)
+    // runs on a side stream concurrently with the psi passes of step n; ib_ahead says
+    // it has been done, so X, Uprev, Xh, F and G already belong to the next step
+    cudaStream_t side;
+    cudaEvent_t ev_fork, ev_join;
+    bool ib_ahead;
+    int lookahead;                    // 1 (default) enables the overlap
+    // CUDA graphs of one regular step, per pointer parity (u <-> st, N <-> G swaps) and
+    // per look-ahead state at entry
     int parity;
     bool use_graphs;
-    cudaGraphExec_t gexec[2];
-    bool gvalid[2];
-    int64_t glaunches[2];             // kernels per captured step
+    cudaGraphExec_t gexec[4];
+    bool gvalid[4];
+    int64_t glaunches[4];             // kernels per captured step
     // per-phase profiling (ib_set_profiling)
     int profiling;
     cudaEvent_t ev[IB_NPHASES][2];
