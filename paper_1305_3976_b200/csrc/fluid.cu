@@ -372,16 +372,24 @@ struct LinePass {
             });
         } else {
             // pure copies: cp.async keeps every load of the tile in flight at once
-            const double* src = (KIND == K_PSI_LAST) ? A.pstar : pick3<double*>(A.io[0], A.io[1], A.io[2], comp);
-            const double* src2 = (KIND == K_LAST) ? pick3<const double*>(A.un[0], A.un[1], A.un[2], comp)
-                                                  : (KIND == K_PSI_LAST ? A.p : nullptr);
-            for_tile<AX>(n, nrow, R, g0, tb, t, T, [&](int l, int m, unsigned q) {
-                const int off = tile_off<L>(l, m, TP);
-                cp_async8(tile + off, src + q);
-                if (KIND == K_LAST || KIND == K_PSI_LAST) cp_async8(tile2 + off, src2 + q);
-            });
+            issue(tile, tile2, A, n, R, TP, g0, tb, comp, t, T);
             cp_async_wait_all();
         }
+    }
+
+    // copy kinds: start the cp.async loads of a tile (the caller commits and waits)
+    static __device__ __forceinline__ void issue(double* tile, double* tile2, const LArgs& A, int n, int R, int TP,
+                                                 int g0, unsigned tb, int comp, int t, int T)
+    {
+        const int nrow = (DIM == 2) ? A.nl : n;
+        const double* src = (KIND == K_PSI_LAST) ? A.pstar : pick3<double*>(A.io[0], A.io[1], A.io[2], comp);
+        const double* src2 = (KIND == K_LAST) ? pick3<const double*>(A.un[0], A.un[1], A.un[2], comp)
+                                              : (KIND == K_PSI_LAST ? A.p : nullptr);
+        for_tile<AX>(n, nrow, R, g0, tb, t, T, [&](int l, int m, unsigned q) {
+            const int off = tile_off<L>(l, m, TP);
+            cp_async8(tile + off, src + q);
+            if (KIND == K_LAST || KIND == K_PSI_LAST) cp_async8(tile2 + off, src2 + q);
+        });
     }
 
     // warp-synchronous solve of the tile's R lines (P lanes per line); w / nw: this
