@@ -56,8 +56,8 @@ def lib():
     """Load libibgm.so (building it first if sources are newer and nvcc exists)."""
     global _lib
     if _lib is None:
-        path = _build.LIB
-        if _build.needs_build():
+        path = os.environ.get("IBGM_LIB_PATH") or _build.LIB     # dev A/B builds only
+        if path == _build.LIB and _build.needs_build():
             try:
                 _build.build()
             except Exception as e:  # noqa: BLE001
