@@ -227,6 +227,9 @@ static void free_lagrangian(Ctx* s)
         cudaFree(s->grp->Upart); cudaFree(s->grp->Ured);
         s->grp->Upart = s->grp->Ured = nullptr;
         s->grp->ucap = 0;
+        for (int r = 0; r < s->grp->nloc; ++r) { cudaFree(s->grp->sel[r]); s->grp->sel[r] = nullptr; }
+        cudaFree(s->grp->sel_cnt);
+        s->grp->sel_cnt = nullptr;
     }
 }
 
@@ -632,6 +635,8 @@ int ib_set_boundary(ib_ctx* c, int64_t npts, const double* X, int64_t nedges, co
         CKC(cudaMalloc(&G->Ured, sizeof(double) * cnt));
         CKC(cudaMemsetAsync(G->Upart, 0, sizeof(double) * cnt * slots, s->stream));
         G->ucap = cnt;
+        for (int r = 0; r < G->nloc; ++r) CKC(cudaMalloc(&G->sel[r], sizeof(int) * npts));
+        CKC(cudaMalloc(&G->sel_cnt, sizeof(int) * G->nloc));
     }
     CKC(cudaStreamSynchronize(s->stream));
     s->npts = npts;
@@ -860,7 +865,7 @@ static int enqueue_step_slab(Ctx* s, int first)
         const int64_t cnt = s->npts * d;
         for (int r = 0; r < G->nloc; ++r) {
             double* part = G->Upart + ((G->transport == IB_TRANSPORT_EMULATE) ? (size_t)r * cnt : 0);
-            CKC(slab_interp_part(s, G->slab[r], part));
+            CKC(slab_interp_part(s, G->slab[r], part, G->sel[r], G->sel_cnt + r));
         }
         CKG(group_allreduce_U(G, s, s->stream));
         // Steps 1b-1c on every rank (identical arithmetic on identical U^n)
@@ -871,7 +876,7 @@ static int enqueue_step_slab(Ctx* s, int first)
         }
         PHASE(IB_PH_FORCE, launch_force(s));
         if (s->profiling) CKC(cudaEventRecord(s->ev[IB_PH_SPREAD][0], s->stream));
-        FOR_SLABS(slab_spread_part(s, sl));
+        for (int r = 0; r < G->nloc; ++r) CKC(slab_spread_part(s, G->slab[r], G->sel[r], G->sel_cnt + r));
         if (s->profiling) {
             CKC(cudaEventRecord(s->ev[IB_PH_SPREAD][1], s->stream));
             s->ph_pending[IB_PH_SPREAD] = true;

@@ -135,6 +135,8 @@ struct Group {
     double* Upart;                    // partial interpolation ([P][npts*d] emulated, [npts*d] NCCL)
     double* Ured;                     // U^n after the sum over ranks
     int64_t ucap;                     // capacity (points*d) of Upart/Ured
+    int* sel[kMaxRanks];              // per local slab: the points whose support meets it
+    int* sel_cnt;                     // [nloc] counters
     double* coef[SYS_COUNT];          // device slab coefficient blocks
     void* comm;                       // ncclComm_t
 };
@@ -156,10 +158,10 @@ cudaError_t slab_divpsi_fwd(Ctx* s, Group* G);
 cudaError_t slab_divpsi_corr(Ctx* s, Group* G);
 cudaError_t slab_user_fwd(Ctx* s, Group* G, double* data, int mf);
 cudaError_t slab_user_corr(Ctx* s, Group* G, double* data, int mf);
-cudaError_t slab_interp_part(Ctx* top, Ctx* s, double* Upart);
+cudaError_t slab_interp_part(Ctx* top, Ctx* s, double* Upart, int* list, int* count);
 cudaError_t slab_sum_slots(Ctx* top, const double* part, int P, double* out);
 cudaError_t slab_evolve(Ctx* top, const double* U, int first);
-cudaError_t slab_spread_part(Ctx* top, Ctx* s);
+cudaError_t slab_spread_part(Ctx* top, Ctx* s, int* list, int* count);
 int group_halo(Group* G, int nf, const HaloSpec* spec, cudaStream_t st);
 int group_allgather(Group* G, cudaStream_t st);
 int group_allreduce_U(Group* G, Ctx* top, cudaStream_t st);

@@ -250,6 +250,14 @@ __global__ void __launch_bounds__(128) k_slab_corr(SlabCf C, SlabArgs A, int slo
 
 static unsigned nb128(long long cnt) { return (unsigned)((cnt + 127) / 128); }
 
+template <int DIM, int SRC, int MF>
+static cudaError_t launch_fwd(Ctx* s, const SlabCf& C, const SlabArgs& a, int ncomp)
+{
+    k_slab_fwd<DIM, SRC, MF><<<dim3(nb128(s->plane), (unsigned)ncomp), 128, 0, s->stream>>>(C, a, 0);
+    s->launches++;
+    return cudaGetLastError();
+}
+
 static SlabArgs slab_args(Ctx* s, Group* G)
 {
     SlabArgs a{};
@@ -270,11 +278,8 @@ cudaError_t slab_sweep_last_fwd(Ctx* s, Group* G)
     SlabArgs a = slab_args(s, G);
     for (int c = 0; c < s->dim; ++c) { a.io[c] = s->st[c]; a.un[c] = s->u[c]; }
     SlabCf C{G->coef[SYS_VISC], (int)s->nl - 1, G->P};
-    dim3 grid(nb128(s->plane), (unsigned)s->dim);
-    if (s->dim == 3) k_slab_fwd<3, SRC_FIELD, 0><<<grid, 128, 0, s->stream>>>(C, a, 0);
-    else k_slab_fwd<2, SRC_FIELD, 0><<<grid, 128, 0, s->stream>>>(C, a, 0);
-    s->launches++;
-    return cudaGetLastError();
+    if (s->dim == 3) return launch_fwd<3, SRC_FIELD, 0>(s, C, a, 3);
+    return launch_fwd<2, SRC_FIELD, 0>(s, C, a, 2);
 }
 
 cudaError_t slab_sweep_last_corr(Ctx* s, Group* G)
@@ -295,10 +300,8 @@ cudaError_t slab_divpsi_fwd(Ctx* s, Group* G)
     for (int c = 0; c < s->dim; ++c) { a.un[c] = s->u[c]; a.unew[c] = s->st[c]; }
     a.p = s->p;
     SlabCf C{G->coef[SYS_PSI], (int)s->nl - 1, G->P};
-    if (s->dim == 3) k_slab_fwd<3, SRC_DIV, 1><<<dim3(nb128(s->plane), 1), 128, 0, s->stream>>>(C, a, 0);
-    else k_slab_fwd<2, SRC_DIV, 1><<<dim3(nb128(s->plane), 1), 128, 0, s->stream>>>(C, a, 0);
-    s->launches++;
-    return cudaGetLastError();
+    if (s->dim == 3) return launch_fwd<3, SRC_DIV, 1>(s, C, a, 1);
+    return launch_fwd<2, SRC_DIV, 1>(s, C, a, 1);
 }
 
 cudaError_t slab_divpsi_corr(Ctx* s, Group* G)
@@ -317,16 +320,12 @@ cudaError_t slab_user_fwd(Ctx* s, Group* G, double* data, int mf)
     SlabArgs a = slab_args(s, G);
     a.io[0] = a.io[1] = a.io[2] = data;
     SlabCf C{G->coef[SYS_USER], (int)s->nl - 1, G->P};
-    const dim3 grid(nb128(s->plane), 1);
     if (mf) {
-        if (s->dim == 3) k_slab_fwd<3, SRC_FIELD, 1><<<grid, 128, 0, s->stream>>>(C, a, 0);
-        else k_slab_fwd<2, SRC_FIELD, 1><<<grid, 128, 0, s->stream>>>(C, a, 0);
-    } else {
-        if (s->dim == 3) k_slab_fwd<3, SRC_FIELD, 0><<<grid, 128, 0, s->stream>>>(C, a, 0);
-        else k_slab_fwd<2, SRC_FIELD, 0><<<grid, 128, 0, s->stream>>>(C, a, 0);
+        if (s->dim == 3) return launch_fwd<3, SRC_FIELD, 1>(s, C, a, 1);
+        return launch_fwd<2, SRC_FIELD, 1>(s, C, a, 1);
     }
-    s->launches++;
-    return cudaGetLastError();
+    if (s->dim == 3) return launch_fwd<3, SRC_FIELD, 0>(s, C, a, 1);
+    return launch_fwd<2, SRC_FIELD, 0>(s, C, a, 1);
 }
 
 cudaError_t slab_user_corr(Ctx* s, Group* G, double* data, int mf)
@@ -374,13 +373,42 @@ __device__ __forceinline__ int wrapp(int i, int n) { return i >= n ? i - n : i; 
 // Step 1a restricted to the nodes this slab owns (global planes z0 .. z0+nz-1 of the
 // last axis): Upart_k = sum over owned stencil nodes of u phi phi (phi).  The sum over
 // ranks (all-reduce) is U^n of PAPER.md:581-586.
+// The points whose 4-point support (any staggering: cells cz-2 .. cz+2 of the last axis)
+// meets this slab's planes, appended to list (warp-aggregated; order irrelevant).
+template <int DIM>
+__global__ void k_slab_select(const double* __restrict__ X, long long npts, int n, int z0, int nz, double invh,
+                              int* __restrict__ list, int* __restrict__ count)
+{
+    const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    bool hit = false;
+    if (k < npts) {
+        const int cz = (int)floor(X[k * DIM + DIM - 1] * invh);
+#pragma unroll
+        for (int d = -2; d <= 2; ++d) {
+            int g = (cz + d) % n;
+            if (g < 0) g += n;
+            hit = hit || (unsigned)(g - z0) < (unsigned)nz;
+        }
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    if (m == 0) return;
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(m) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(count, __popc(m));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (hit) list[base + __popc(m & ((1u << lane) - 1u))] = (int)k;
+}
+
 template <int DIM, int KER>
 __global__ void k_interp_part(const double* __restrict__ u0, const double* __restrict__ u1,
                               const double* __restrict__ u2, const double* __restrict__ X,
-                              double* __restrict__ Upart, long long npts, int n, int z0, int nz, double invh)
+                              double* __restrict__ Upart, const int* __restrict__ list, const int* __restrict__ count,
+                              int n, int z0, int nz, double invh)
 {
-    const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (k >= npts) return;
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= *count) return;
+    const long long k = list[i];
     double Xk[3];
 #pragma unroll
     for (int a = 0; a < DIM; ++a) Xk[a] = X[k * DIM + a];
@@ -446,11 +474,13 @@ __global__ void k_evolve(const double* __restrict__ U, double* __restrict__ X, d
 template <int DIM, int KER, bool KEEP>
 __global__ void __launch_bounds__(128) k_spread_part(const double* __restrict__ Xh, const double* __restrict__ F,
                                                      const double* __restrict__ wgt, double* g0, double* g1, double* g2,
-                                                     double* f0, double* f1, double* f2, long long npts, int n, int z0,
+                                                     double* f0, double* f1, double* f2, const int* __restrict__ list,
+                                                     const int* __restrict__ count, int n, int z0,
                                                      int nz, double invh, double invhd, double two_rho)
 {
-    const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (k >= npts) return;
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= *count) return;
+    const long long k = list[i];
     double Xk[3];
 #pragma unroll
     for (int a = 0; a < DIM; ++a) Xk[a] = Xh[k * DIM + a];
@@ -498,11 +528,30 @@ __global__ void __launch_bounds__(128) k_spread_part(const double* __restrict__ 
     }
 }
 
-cudaError_t slab_interp_part(Ctx* top, Ctx* s, double* Upart)
+// select the points of slab s (list r of the group) from positions Xsrc
+static cudaError_t slab_select(Ctx* top, Ctx* s, const double* Xsrc, int* list, int* count)
+{
+    cudaError_t e = cudaMemsetAsync(count, 0, sizeof(int), s->stream);
+    if (e != cudaSuccess) return e;
+    const double invh = 1.0 / s->h;
+    if (s->dim == 3)
+        k_slab_select<3><<<nb128(top->npts), 128, 0, s->stream>>>(Xsrc, top->npts, (int)s->n, (int)s->z0, (int)s->nl,
+                                                                  invh, list, count);
+    else
+        k_slab_select<2><<<nb128(top->npts), 128, 0, s->stream>>>(Xsrc, top->npts, (int)s->n, (int)s->z0, (int)s->nl,
+                                                                  invh, list, count);
+    s->launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t slab_interp_part(Ctx* top, Ctx* s, double* Upart, int* list, int* count)
 {
     const double invh = 1.0 / s->h;
+    cudaError_t e = cudaMemsetAsync(Upart, 0, sizeof(double) * top->npts * top->dim, s->stream);
+    if (e != cudaSuccess) return e;
+    if ((e = slab_select(top, s, top->X, list, count)) != cudaSuccess) return e;
 #define IBGM_IP(D, K) k_interp_part<D, K><<<nb128(top->npts), 128, 0, s->stream>>>( \
-        s->u[0], s->u[1], s->u[2], top->X, Upart, top->npts, (int)s->n, (int)s->z0, (int)s->nl, invh)
+        s->u[0], s->u[1], s->u[2], top->X, Upart, list, count, (int)s->n, (int)s->z0, (int)s->nl, invh)
     if (s->dim == 2) { if (top->kernel == IB_DELTA_COS4) IBGM_IP(2, 0); else IBGM_IP(2, 1); }
     else { if (top->kernel == IB_DELTA_COS4) IBGM_IP(3, 0); else IBGM_IP(3, 1); }
 #undef IBGM_IP
@@ -526,13 +575,15 @@ cudaError_t slab_evolve(Ctx* top, const double* U, int first)
     return cudaGetLastError();
 }
 
-cudaError_t slab_spread_part(Ctx* top, Ctx* s)
+cudaError_t slab_spread_part(Ctx* top, Ctx* s, int* list, int* count)
 {
     const double invh = 1.0 / s->h;
     const double invhd = (s->dim == 3) ? invh * invh * invh : invh * invh;
     const bool kp = top->debug_keep_f != 0;
-#define IBGM_SPP(D, K, KP) k_spread_part<D, K, KP><<<nb128(top->npts), 128, 0, s->stream>>>(                       \
-        top->Xh, top->F, top->wgt, s->nprev[0], s->nprev[1], s->nprev[2], s->f[0], s->f[1], s->f[2], top->npts, \
+    cudaError_t e = slab_select(top, s, top->Xh, list, count);
+    if (e != cudaSuccess) return e;
+#define IBGM_SPP(D, K, KP) k_spread_part<D, K, KP><<<nb128(top->npts), 128, 0, s->stream>>>(                  \
+        top->Xh, top->F, top->wgt, s->nprev[0], s->nprev[1], s->nprev[2], s->f[0], s->f[1], s->f[2], list, count, \
         (int)s->n, (int)s->z0, (int)s->nl, invh, invhd, 2.0 / s->rho)
     if (s->dim == 2) {
         if (top->kernel == IB_DELTA_COS4) { if (kp) IBGM_SPP(2, 0, true); else IBGM_SPP(2, 0, false); }

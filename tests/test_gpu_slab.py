@@ -207,3 +207,24 @@ def test_ellipse_array_points_cross_slabs():
     # the background flow carried the membranes by ~30 dt |u| = 0.3 h
     assert np.abs(fg["X"] - pr.X).max() > 0.1 / 32
     g.close(); g1.close()
+
+
+@pytest.mark.slow
+def test_config4_full_size_eight_slabs_matches_single_gpu():
+    """Config 4 at full size (384^3, 8 x 100k-node shells, the 8-GPU workload of
+    BASELINE.json) cut into 8 z-slabs of 48 planes (EMULATE): 10 steps equal the
+    single-GPU path to 1e-10 (the oracle's full-size check is the single-GPU one,
+    test_config4_full_size_one_step)."""
+    from paper_1305_3976_b200 import inputs
+    pr = inputs.config(4)
+    g1 = _gpu(pr, 1)
+    g1.step(10)
+    f1 = g1.fields()
+    g1.close()
+    g = _gpu(pr, 8)
+    g.step(10)
+    fg = g.fields()
+    g.close()
+    for c in range(3):
+        assert _rel(fg["u"][c], f1["u"][c]) <= 1e-10, c
+    assert _rel(fg["p"], f1["p"]) <= 1e-10 and _rel(fg["X"], f1["X"]) <= 1e-10

@@ -23,7 +23,9 @@ def run(cfg, steps=50, **over):
     tg = time.time() - t0
     st = torch.cuda.Stream()
     torch.cuda.set_stream(st)
-    ctx = ibgm.from_problem(pr, stream=st.cuda_stream)
+    P = int(os.environ.get("SLAB_P", "1"))
+    kw = dict(nranks=P, transport=ibgm.IB_TRANSPORT_EMULATE) if P > 1 else {}
+    ctx = ibgm.from_problem(pr, stream=st.cuda_stream, **kw)
     ctx.set_debug(False, MODE, IMODE)
     ctx.step(5)
     ctx.sync()
