@@ -300,7 +300,7 @@ static int64_t total_launches(Ctx* s)
 static int upload_coef(Ctx* s, int sys, double c, double a, double b, int mf)
 {
     Group* G = s->grp;
-    std::vector<double> v = slab_coef_block(s->n, (int)(s->n / G->P), c, a, b, mf);
+    std::vector<double> v = slab_coef_block(s->n, (int)(s->n / (G->P * G->Q)), c, a, b, mf);
     if (G->coef[sys]) cudaFree(G->coef[sys]);
     G->coef[sys] = nullptr;
     CKC(cudaMalloc(&G->coef[sys], v.size() * sizeof(double)));
@@ -479,8 +479,21 @@ int ib_create(const ib_grid* grid, double nu, double rho, double dt, const ib_op
             G->slab[r] = sl;
             CKC(alloc_fields(sl));
         }
-        CKC(cudaMalloc(&G->gather, sizeof(double) * (size_t)P * kSlabSlots * s->plane));
-        CKC(cudaMemsetAsync(G->gather, 0, sizeof(double) * (size_t)P * kSlabSlots * s->plane, s->stream));
+        // Schur parts per slab: the smallest divisor Q of nz that gives >= 64k threads per
+        // cut-axis pass (a slab is then Q consecutive parts of every line; R29)
+        G->Q = 1;
+        while (G->Q < nz && ((int64_t)s->plane * G->Q < 65536 || nz % G->Q != 0)) {
+            ++G->Q;
+            while (G->Q < nz && nz % G->Q != 0) ++G->Q;
+            if ((int64_t)s->plane * G->Q >= 65536) break;
+        }
+        if (nz / G->Q < 2) G->Q = nz / 2;
+        if (G->Q * P > 128) G->Q = 128 / P > 0 ? 128 / P : 1;   // the reduced system stays <= 128 parts
+        if (G->Q < 1) G->Q = 1;
+        while (nz % G->Q != 0) --G->Q;
+        const size_t gsz = sizeof(double) * (size_t)P * G->Q * kSlabSlots * s->plane;
+        CKC(cudaMalloc(&G->gather, gsz));
+        CKC(cudaMemsetAsync(G->gather, 0, gsz, s->stream));
         int rc;
         if ((rc = upload_coef(s, SYS_VISC, -kv, 1.0 + 2.0 * kv, -kv, 0)) != IB_OK) return rc;
         if ((rc = upload_coef(s, SYS_PSI, -kp, 1.0 + 2.0 * kp, -kp, 1)) != IB_OK) return rc;

@@ -130,8 +130,9 @@ struct Group {
     int transport;                    // IB_TRANSPORT_EMULATE | IB_TRANSPORT_NCCL
     int rank;                         // NCCL: this process's rank
     int nloc;                         // slabs held by this context (P emulated, 1 with NCCL)
+    int Q;                            // Schur parts per slab along the cut axis (nz = Q Lseg)
     Ctx* slab[kMaxRanks];
-    double* gather;                   // [P][kSlabSlots][plane]
+    double* gather;                   // [P Q][kSlabSlots][plane]
     double* Upart;                    // partial interpolation ([P][npts*d] emulated, [npts*d] NCCL)
     double* Ured;                     // U^n after the sum over ranks
     int64_t ucap;                     // capacity (points*d) of Upart/Ured

@@ -126,6 +126,7 @@ struct SlabArgs {
     double* gather;           // [P][kSlots][plane]
     double neg_rho_dt, chimu_half, invh;
     int n, nz, rank;
+    int Q, Lseg;              // Schur parts per slab and their length (nz = Q Lseg)
     long long plane;          // N^{d-1}
 };
 
@@ -138,7 +139,9 @@ __global__ void __launch_bounds__(128) k_slab_fwd(SlabCf C, SlabArgs A, int slot
     const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (q >= A.plane) return;
     const int comp = blockIdx.y;
-    double* io = (comp == 0) ? A.io[0] : (comp == 1 ? A.io[1] : A.io[2]);
+    const int k0 = blockIdx.z * A.Lseg;                  // first plane of this Schur part
+    const int part = A.rank * A.Q + blockIdx.z;          // its index along the whole line
+    double* io = ((comp == 0) ? A.io[0] : (comp == 1 ? A.io[1] : A.io[2])) + (long long)k0 * A.plane;
     const long long PL = A.plane;
     const int n = A.n;
     long long off[3] = {1, n, PL};      // +e_x, +e_y, +e_last (periodic in x, y within the slab)
@@ -158,15 +161,16 @@ __global__ void __launch_bounds__(128) k_slab_fwd(SlabCf C, SlabArgs A, int slot
         // Step 3e RHS r = -(rho/dt) D.u^{n+1} and the explicit part of Step 3f
         // (PAPER.md:484-491, 668-683); the +e_last neighbour of plane nz-1 is the halo
         double dn = 0.0, dol = 0.0;
+        const long long fg = f + (long long)k0 * PL;   // offset in the slab fields
 #pragma unroll
         for (int c = 0; c < DIM; ++c) {
             const long long o = (c == DIM - 1) ? PL : off[c];
-            dn += A.unew[c][f + o] - A.unew[c][f];
-            dol += A.un[c][f + o] - A.un[c][f];
+            dn += A.unew[c][fg + o] - A.unew[c][fg];
+            dol += A.un[c][fg + o] - A.un[c][fg];
         }
         dn *= A.invh;
         dol *= A.invh;
-        A.p[f] = A.p[f] - A.chimu_half * (dn + dol);
+        A.p[fg] = A.p[fg] - A.chimu_half * (dn + dol);
         const double r = A.neg_rho_dt * dn;
         io[f] = r;
         return r;
@@ -190,7 +194,7 @@ __global__ void __launch_bounds__(128) k_slab_fwd(SlabCf C, SlabArgs A, int slot
         io[i * PL + q] = x;
         fsum += x;
     }
-    double* g = A.gather + ((long long)A.rank * kSlabSlots + slot0 + 2 * comp) * PL;
+    double* g = A.gather + ((long long)part * kSlabSlots + slot0 + 2 * comp) * PL;
     g[q] = d0 - b * x;                  // x = f*_1 here
     g[PL + q] = fm;
     if (MF) {
@@ -209,10 +213,12 @@ __global__ void __launch_bounds__(128) k_slab_corr(SlabCf C, SlabArgs A, int slo
     const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (q >= A.plane) return;
     const int comp = blockIdx.y;
-    double* io = (comp == 0) ? A.io[0] : (comp == 1 ? A.io[1] : A.io[2]);
-    const double* un = (comp == 0) ? A.un[0] : (comp == 1 ? A.un[1] : A.un[2]);
+    const long long k0 = (long long)blockIdx.z * A.Lseg;
+    const int part = A.rank * A.Q + blockIdx.z;
+    double* io = ((comp == 0) ? A.io[0] : (comp == 1 ? A.io[1] : A.io[2])) + k0 * A.plane;
+    const double* un = ((comp == 0) ? A.un[0] : (comp == 1 ? A.un[1] : A.un[2])) + k0 * A.plane;
     const long long PL = A.plane;
-    const int P = C.P, s = A.rank, s1 = (A.rank + 1) % C.P;
+    const int P = C.P, s = part, s1 = (part + 1) % C.P;
     slot0 += 2 * comp;                  // component c uses slots slot0 + 2c, slot0 + 2c + 1
     const double c = C.c(), b = C.b();
     const double* SI = C.sinv();
@@ -253,7 +259,7 @@ static unsigned nb128(long long cnt) { return (unsigned)((cnt + 127) / 128); }
 template <int DIM, int SRC, int MF>
 static cudaError_t launch_fwd(Ctx* s, const SlabCf& C, const SlabArgs& a, int ncomp)
 {
-    k_slab_fwd<DIM, SRC, MF><<<dim3(nb128(s->plane), (unsigned)ncomp), 128, 0, s->stream>>>(C, a, 0);
+    k_slab_fwd<DIM, SRC, MF><<<dim3(nb128(s->plane), (unsigned)ncomp, (unsigned)a.Q), 128, 0, s->stream>>>(C, a, 0);
     s->launches++;
     return cudaGetLastError();
 }
@@ -265,6 +271,8 @@ static SlabArgs slab_args(Ctx* s, Group* G)
     a.n = (int)s->n;
     a.nz = (int)s->nl;
     a.rank = s->rank;
+    a.Q = G->Q;
+    a.Lseg = (int)(s->nl / G->Q);
     a.plane = s->plane;
     a.invh = 1.0 / s->h;
     a.neg_rho_dt = -s->rho / s->dt;
@@ -277,7 +285,7 @@ cudaError_t slab_sweep_last_fwd(Ctx* s, Group* G)
 {
     SlabArgs a = slab_args(s, G);
     for (int c = 0; c < s->dim; ++c) { a.io[c] = s->st[c]; a.un[c] = s->u[c]; }
-    SlabCf C{G->coef[SYS_VISC], (int)s->nl - 1, G->P};
+    SlabCf C{G->coef[SYS_VISC], (int)(s->nl / G->Q) - 1, G->P * G->Q};
     if (s->dim == 3) return launch_fwd<3, SRC_FIELD, 0>(s, C, a, 3);
     return launch_fwd<2, SRC_FIELD, 0>(s, C, a, 2);
 }
@@ -286,8 +294,8 @@ cudaError_t slab_sweep_last_corr(Ctx* s, Group* G)
 {
     SlabArgs a = slab_args(s, G);
     for (int c = 0; c < s->dim; ++c) { a.io[c] = s->st[c]; a.un[c] = s->u[c]; }
-    SlabCf C{G->coef[SYS_VISC], (int)s->nl - 1, G->P};
-    k_slab_corr<EPI_ADD_UN, 0><<<dim3(nb128(s->plane), (unsigned)s->dim), 128, 0, s->stream>>>(C, a, 0);
+    SlabCf C{G->coef[SYS_VISC], (int)(s->nl / G->Q) - 1, G->P * G->Q};
+    k_slab_corr<EPI_ADD_UN, 0><<<dim3(nb128(s->plane), (unsigned)s->dim, (unsigned)a.Q), 128, 0, s->stream>>>(C, a, 0);
     s->launches++;
     return cudaGetLastError();
 }
@@ -299,7 +307,7 @@ cudaError_t slab_divpsi_fwd(Ctx* s, Group* G)
     a.io[0] = a.io[1] = a.io[2] = s->pstar;
     for (int c = 0; c < s->dim; ++c) { a.un[c] = s->u[c]; a.unew[c] = s->st[c]; }
     a.p = s->p;
-    SlabCf C{G->coef[SYS_PSI], (int)s->nl - 1, G->P};
+    SlabCf C{G->coef[SYS_PSI], (int)(s->nl / G->Q) - 1, G->P * G->Q};
     if (s->dim == 3) return launch_fwd<3, SRC_DIV, 1>(s, C, a, 1);
     return launch_fwd<2, SRC_DIV, 1>(s, C, a, 1);
 }
@@ -308,8 +316,8 @@ cudaError_t slab_divpsi_corr(Ctx* s, Group* G)
 {
     SlabArgs a = slab_args(s, G);
     a.io[0] = a.io[1] = a.io[2] = s->pstar;
-    SlabCf C{G->coef[SYS_PSI], (int)s->nl - 1, G->P};
-    k_slab_corr<EPI_STORE, 1><<<dim3(nb128(s->plane), 1), 128, 0, s->stream>>>(C, a, 0);
+    SlabCf C{G->coef[SYS_PSI], (int)(s->nl / G->Q) - 1, G->P * G->Q};
+    k_slab_corr<EPI_STORE, 1><<<dim3(nb128(s->plane), 1, (unsigned)a.Q), 128, 0, s->stream>>>(C, a, 0);
     s->launches++;
     return cudaGetLastError();
 }
@@ -319,7 +327,7 @@ cudaError_t slab_user_fwd(Ctx* s, Group* G, double* data, int mf)
 {
     SlabArgs a = slab_args(s, G);
     a.io[0] = a.io[1] = a.io[2] = data;
-    SlabCf C{G->coef[SYS_USER], (int)s->nl - 1, G->P};
+    SlabCf C{G->coef[SYS_USER], (int)(s->nl / G->Q) - 1, G->P * G->Q};
     if (mf) {
         if (s->dim == 3) return launch_fwd<3, SRC_FIELD, 1>(s, C, a, 1);
         return launch_fwd<2, SRC_FIELD, 1>(s, C, a, 1);
@@ -332,8 +340,8 @@ cudaError_t slab_user_corr(Ctx* s, Group* G, double* data, int mf)
 {
     SlabArgs a = slab_args(s, G);
     a.io[0] = a.io[1] = a.io[2] = data;
-    SlabCf C{G->coef[SYS_USER], (int)s->nl - 1, G->P};
-    const dim3 grid(nb128(s->plane), 1);
+    SlabCf C{G->coef[SYS_USER], (int)(s->nl / G->Q) - 1, G->P * G->Q};
+    const dim3 grid(nb128(s->plane), 1, (unsigned)a.Q);
     if (mf) k_slab_corr<EPI_STORE, 1><<<grid, 128, 0, s->stream>>>(C, a, 0);
     else k_slab_corr<EPI_STORE, 0><<<grid, 128, 0, s->stream>>>(C, a, 0);
     s->launches++;
@@ -656,7 +664,7 @@ int group_halo(Group* G, int nf, const HaloSpec* spec, cudaStream_t st)
 int group_allgather(Group* G, cudaStream_t st)
 {
     if (G->transport == IB_TRANSPORT_EMULATE) return 0;
-    const size_t cnt = (size_t)kSlabSlots * G->slab[0]->plane;
+    const size_t cnt = (size_t)G->Q * kSlabSlots * G->slab[0]->plane;   // this rank's Q parts
     return g_nccl.AllGather(G->gather + (size_t)G->rank * cnt, G->gather, cnt, kNcclDouble, G->comm, st);
 }
 
