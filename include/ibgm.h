@@ -66,7 +66,8 @@ typedef struct ib_ctx ib_ctx; /* opaque; owned by the library until ib_destroy *
 typedef struct {
     int32_t dim; /* 2 or 3 */
     int64_t n;   /* cells per side N; must have a divisor L in {2,3,4,6,8,12,16,24,32}
-                    with N/L <= 32 (line-solve segmentation), 8 <= N <= 1024           */
+                    (or 64, 128 in 2D) with N/L <= 32 (line-solve segmentation);
+                    8 <= N <= 1024 in 3D, <= 4096 in 2D                                */
     double H;    /* box side H > 0 (1 in every BASELINE config); h = H/N in every
                     operator, including the literal psi operator (1 - D_aa),
                     D_aa = delta_aa/h^2 (R2); positions live in [0, H)^d */

@@ -135,7 +135,8 @@ static void schur_factors(int64_t N, int L, long double c, long double a, long d
         for (int p = 0; p < P; ++p) F->colsum[q] += I[(size_t)p * P + q];
 }
 
-void make_line_coef(LineCoef* C, SchurInv* SI, int64_t N, int L, double c_, double a_, double b_, int mean_fix)
+void make_line_coef(LineCoef* C, SchurInv* SI, int64_t N, int L, double c_, double a_, double b_, int mean_fix,
+                    double* ext_host)
 {
     memset(C, 0, sizeof(*C));
     memset(SI, 0, sizeof(*SI));
@@ -145,10 +146,17 @@ void make_line_coef(LineCoef* C, SchurInv* SI, int64_t N, int L, double c_, doub
     C->L = L; C->P = F.P; C->N = (int)N; C->mean_fix = mean_fix;
     C->inv_rowsum = (double)(1.0L / ((long double)a_ + b_ + c_));
     for (int i = 0; i < F.m; ++i) {
-        C->inv[i] = (double)F.inv[i];
-        C->cp[i] = (double)F.cp[i];
-        C->g[i] = (double)F.g[i];
-        C->h[i] = (double)F.h[i];
+        if (L <= kMaxL) {
+            C->inv[i] = (double)F.inv[i];
+            C->cp[i] = (double)F.cp[i];
+            C->g[i] = (double)F.g[i];
+            C->h[i] = (double)F.h[i];
+        } else if (ext_host) {
+            ext_host[i] = (double)F.inv[i];
+            ext_host[F.m + i] = (double)F.cp[i];
+            ext_host[2 * F.m + i] = (double)F.g[i];
+            ext_host[3 * F.m + i] = (double)F.h[i];
+        }
     }
     C->gsum = (double)F.gsum;
     C->hsum = (double)F.hsum;
@@ -188,7 +196,9 @@ static std::vector<double> slab_coef_block(int64_t N, int nz, double c, double a
 
 static bool choose_segmentation(int64_t n, int* L, int* P)
 {
-    static const int cands[] = {8, 12, 16, 24, 32, 6, 4, 3, 2};
+    // N <= 1024: segments of <= 32 unknowns (registers); 2D N in {2048, 4096}: 32 segments
+    // of 64 / 128 unknowns solved in shared memory
+    static const int cands[] = {8, 12, 16, 24, 32, 6, 4, 3, 2, 64, 128};
     for (int c : cands) {
         if (n % c == 0 && n / c <= kMaxSeg) {
             *L = c;
@@ -367,7 +377,8 @@ int ib_create(const ib_grid* grid, double nu, double rho, double dt, const ib_op
     ib_options o;
     if (opt) o = *opt; else ib_default_options(&o);
     if (grid->dim != 2 && grid->dim != 3) return fail(IB_EINVAL, "dim must be 2 or 3 (got %d)", grid->dim);
-    if (grid->n < 8 || grid->n > 1024) return fail(IB_EINVAL, "N must be in [8, 1024] (got %lld)", (long long)grid->n);
+    if (grid->n < 8 || grid->n > (grid->dim == 2 ? 4096 : 1024))
+        return fail(IB_EINVAL, "N must be in [8, %d] (got %lld)", grid->dim == 2 ? 4096 : 1024, (long long)grid->n);
     if (!(grid->H > 0)) return fail(IB_EINVAL, "the box side H must be > 0");
     if (!(dt > 0) || !(rho > 0) || !(nu >= 0)) return fail(IB_EINVAL, "need dt > 0, rho > 0, nu >= 0");
     if (!(o.chi > 0 && o.chi <= 1)) return fail(IB_EINVAL, "chi must be in (0, 1]");
@@ -389,7 +400,7 @@ int ib_create(const ib_grid* grid, double nu, double rho, double dt, const ib_op
     }
     int L, Pseg;
     if (!choose_segmentation(grid->n, &L, &Pseg))
-        return fail(IB_EINVAL, "N = %lld has no divisor L in {2,3,4,6,8,12,16,24,32} with N/L <= 32",
+        return fail(IB_EINVAL, "N = %lld has no divisor L in {2,...,32, 64, 128} with N/L <= 32",
                     (long long)grid->n);
 
     ib_ctx* c = new ib_ctx();
@@ -427,11 +438,21 @@ int ib_create(const ib_grid* grid, double nu, double rho, double dt, const ib_op
     // viscous Douglas sweeps: (1 - kap delta) with kap = mu dt / (2 rho h^2)
     const double kv = s->mu * dt / (2.0 * rho * s->h * s->h);
     // (well conditioned, cond <= 1 + 4 kv: no mean correction needed, R16)
-    make_line_coef(&s->hcoef[SYS_VISC], &hs[SYS_VISC], s->n, L, -kv, 1.0 + 2.0 * kv, -kv, 0);
-    // psi factors: (1 - D_aa) with D_aa = delta / h^2 (R2)
     const double kp = 1.0 / (s->h * s->h);
-    make_line_coef(&s->hcoef[SYS_PSI], &hs[SYS_PSI], s->n, L, -kp, 1.0 + 2.0 * kp, -kp, 1);
-    make_line_coef(&s->hcoef[SYS_USER], &hs[SYS_USER], s->n, L, -kv, 1.0 + 2.0 * kv, -kv, 0);
+    {
+        // psi factors: (1 - D_aa) with D_aa = delta / h^2 (R2)
+        const double cc[SYS_COUNT] = {-kv, -kp, -kv};
+        const int mfx[SYS_COUNT] = {0, 1, 0};
+        std::vector<double> ext((size_t)4 * (L - 1) + 1);
+        for (int k = 0; k < SYS_COUNT; ++k) {
+            make_line_coef(&s->hcoef[k], &hs[k], s->n, L, cc[k], 1.0 - 2.0 * cc[k], cc[k], mfx[k], ext.data());
+            if (L > kMaxL) {
+                CKC(cudaMalloc(&s->lcext[k], ext.size() * sizeof(double)));
+                CKC(cudaMemcpy(s->lcext[k], ext.data(), ext.size() * sizeof(double), cudaMemcpyHostToDevice));
+                s->hcoef[k].ext = s->lcext[k];
+            }
+        }
+    }
     CKC(cudaMemcpyAsync(s->sinv, hs, sizeof(SchurInv) * SYS_COUNT, cudaMemcpyHostToDevice, s->stream));
 
     if (!slab) {
@@ -1080,7 +1101,12 @@ int ib_line_solve(ib_ctx* c, int32_t axis, double kappa, const double* d, double
         return IB_OK;
     }
     static SchurInv hs;
-    make_line_coef(&s->hcoef[SYS_USER], &hs, s->n, s->L, -kappa, 1.0 + 2.0 * kappa, -kappa, mf);
+    std::vector<double> ext((size_t)4 * (s->L - 1) + 1);
+    make_line_coef(&s->hcoef[SYS_USER], &hs, s->n, s->L, -kappa, 1.0 + 2.0 * kappa, -kappa, mf, ext.data());
+    if (s->L > kMaxL) {
+        CKC(cudaMemcpy(s->lcext[SYS_USER], ext.data(), ext.size() * sizeof(double), cudaMemcpyHostToDevice));
+        s->hcoef[SYS_USER].ext = s->lcext[SYS_USER];
+    }
     const size_t fb = (size_t)s->ncell * sizeof(double);
     CKC(cudaMemcpyAsync(s->sinv + SYS_USER, &hs, sizeof(SchurInv), cudaMemcpyHostToDevice, s->stream));
     CKC(cudaMemcpyAsync(s->tmp, d, fb, cudaMemcpyHostToDevice, s->stream));
@@ -1185,6 +1211,7 @@ int ib_destroy(ib_ctx* c)
         free_lagrangian(s);
     }
     cudaFree(s->sinv);
+    for (int k = 0; k < SYS_COUNT; ++k) cudaFree(s->lcext[k]);
     cudaFree(s->bin_count); cudaFree(s->bin_start); cudaFree(s->bin_cursor); cudaFree(s->bin_list);
     cudaFree(s->bin_nlist); cudaFree(s->bin_partial);
     if (s->ev_made)

@@ -141,6 +141,58 @@ __device__ __forceinline__ void ws_solve(double (&x)[L], const LineCoef& C, int 
 }
 
 // -------------------------------------------------------------------------------
+// The same solve for long segments (L = 64, 128: 2D N = 2048, 4096), run directly on the
+// lane's segment of the shared tile (no register array) with the factors in C.ext.
+// -------------------------------------------------------------------------------
+template <int L>
+__device__ __forceinline__ void ws_solve_smem(double* x, const LineCoef& C, int s, int P, int gbase,
+                                              const double* __restrict__ sinvT)
+{
+    constexpr int M = L - 1;
+    const double c = C.c, b = C.b;
+    const bool mf = C.mean_fix != 0;
+    const double* inv = C.ext;
+    const double* cpv = C.ext + M;
+    const double* gv = C.ext + 2 * M;
+    const double* hv = C.ext + 3 * M;
+    double dsum = 0.0;
+    if (mf)
+        for (int i = 0; i < L; ++i) dsum += x[i];
+    // Thomas on the interior block
+    double prev = x[1] * __ldg(inv);
+    x[1] = prev;
+    for (int i = 2; i <= M; ++i) {
+        prev = (x[i] - c * prev) * __ldg(inv + i - 1);
+        x[i] = prev;
+    }
+    for (int i = M - 1; i >= 1; --i) {
+        prev = x[i] - __ldg(cpv + i - 1) * prev;
+        x[i] = prev;
+    }
+    const int sprev = gbase + ((s == 0) ? P - 1 : s - 1);
+    const int snext = gbase + ((s == P - 1) ? 0 : s + 1);
+    const double fl_prev = __shfl_sync(kFull, x[M], sprev);
+    const double r = x[0] - c * fl_prev - b * x[1];
+    double ys = 0.0;
+    for (int q = 0; q < P; ++q) ys = fma(sinvT[q * P + s], __shfl_sync(kFull, r, gbase + q), ys);
+    const double ys1 = __shfl_sync(kFull, ys, snext);
+    x[0] = ys;
+    const double cy = c * ys, by = b * ys1;
+    double xs = ys;
+    for (int i = 1; i <= M; ++i) {
+        const double v = x[i] - (cy * __ldg(gv + i - 1) + by * __ldg(hv + i - 1));
+        x[i] = v;
+        xs += v;
+    }
+    if (mf) {
+        const double D = group_sum<0>(dsum, P, gbase);
+        const double X = group_sum<0>(xs, P, gbase);
+        const double corr = (D * C.inv_rowsum - X) * C.inv_n;
+        for (int i = 0; i < L; ++i) x[i] += corr;
+    }
+}
+
+// -------------------------------------------------------------------------------
 // S1: all components of  d = u* - u^n  at one cell (Steps 3a-3b)
 // -------------------------------------------------------------------------------
 struct S1Args {
@@ -400,6 +452,14 @@ struct LinePass {
         const int P = C.P;
         const unsigned RTP = (unsigned)R * TP;
         const int lane = threadIdx.x & 31;
+        if constexpr (L > kMaxL) {
+            // long segments: P = 32 lanes = one line per warp, solved in place in the tile
+            for (int l = w; l < R; l += nw)
+#pragma unroll 1
+                for (int c = 0; c < NC; ++c)
+                    ws_solve_smem<L>(tile + c * RTP + l * TP + lane * (L + 1), C, lane, P, 0, sinvT);
+            return;
+        }
         const int lpw = (P <= 32) ? 32 / P : 1;          // lines per warp per round
         const int sub = lane / P;
         const int s = lane - sub * P;
@@ -507,7 +567,9 @@ static int pick_r(const Ctx* s, int L, int nc)
     if (forced == 8 || forced == 16 || forced == 32) return forced;
     for (int R = 32; R >= 8; R /= 2)
         if (lines_smem(s->P, L, nc, R) <= 100 * 1024) return R;
-    return 8;
+    for (int R = 4; R >= 1; R /= 2)     // long segments (2D N > 1024)
+        if (lines_smem(s->P, L, nc, R) <= 200 * 1024) return R;
+    return 1;
 }
 
 template <int L, int KIND, int DIM, int AX, int NC, int MINB>
@@ -544,6 +606,13 @@ static cudaError_t go_lines_k(Ctx* s, int sys, const LArgs& la, int ncomp_grid, 
     return cudaGetLastError();
 }
 
+#define IBGM_DISPATCH_L2D(Lval, CALL)                    \
+    switch (Lval) {                                      \
+        case 64: { constexpr int LL = 64; return CALL; } \
+        case 128: { constexpr int LL = 128; return CALL; } \
+        default: IBGM_DISPATCH_L(Lval, CALL)              \
+    }
+
 #define IBGM_DISPATCH_L(Lval, CALL)                      \
     switch (Lval) {                                      \
         case 2: { constexpr int LL = 2; return CALL; }   \
@@ -567,8 +636,8 @@ static cudaError_t go_axis(Ctx* s, int sys, int axis, const LArgs& a, int ncomp)
         if (axis == 1) { IBGM_DISPATCH_L(s->L, (go_lines<LL, KIND, 3, 1, 1>(s, sys, a, ncomp))) }
         IBGM_DISPATCH_L(s->L, (go_lines<LL, KIND, 3, 2, 1>(s, sys, a, ncomp)))
     }
-    if (axis == 0) { IBGM_DISPATCH_L(s->L, (go_lines<LL, KIND, 2, 0, 1>(s, sys, a, ncomp))) }
-    IBGM_DISPATCH_L(s->L, (go_lines<LL, KIND, 2, 1, 1>(s, sys, a, ncomp)))
+    if (axis == 0) { IBGM_DISPATCH_L2D(s->L, (go_lines<LL, KIND, 2, 0, 1>(s, sys, a, ncomp))) }
+    IBGM_DISPATCH_L2D(s->L, (go_lines<LL, KIND, 2, 1, 1>(s, sys, a, ncomp)))
 }
 
 cudaError_t launch_s1_x(Ctx* s, int first_step)
@@ -583,7 +652,7 @@ cudaError_t launch_s1_x(Ctx* s, int first_step)
     b.a1 = first_step ? 1.0 : 1.5;
     b.first = first_step; b.advection = s->advection;
     if (s->dim == 3) { IBGM_DISPATCH_L(s->L, (go_lines<LL, K_S1, 3, 0, 3>(s, SYS_VISC, a, 1))) }
-    IBGM_DISPATCH_L(s->L, (go_lines<LL, K_S1, 2, 0, 2>(s, SYS_VISC, a, 1)))
+    IBGM_DISPATCH_L2D(s->L, (go_lines<LL, K_S1, 2, 0, 2>(s, SYS_VISC, a, 1)))
 }
 
 cudaError_t launch_sweep_mid(Ctx* s, int axis)

@@ -25,6 +25,7 @@ struct LineCoef {
     double gsum, hsum;        // sum_i g_i, sum_i h_i
     double inv_n;             // 1/N
     int L, P, N, mean_fix;
+    const double* ext;        // L > kMaxL (2D N > 1024): device inv, cp, g, h [m each]
     double inv[kMaxL];        // Thomas: 1/den_i of B (i = 0..m-1)
     double cp[kMaxL];         // Thomas: b/den_i
     double g[kMaxL];          // B^{-1} e_1   (first column of B^{-1})
@@ -67,6 +68,7 @@ struct Ctx {
     double* pstar;                    // p* = p^{n-1/2} + psi^{n-1/2}; psi factors mid-step
     double* tmp;                      // scratch field (ib_get_fields psi, ib_line_solve)
     SchurInv* sinv;                   // device, SYS_COUNT entries
+    double* lcext[SYS_COUNT];         // device long-segment factors (LineCoef::ext)
     LineCoef hcoef[SYS_COUNT];        // host copies (passed by value)
     // Lagrangian state (device)
     int64_t npts, nedges;
@@ -168,7 +170,8 @@ int group_allgather(Group* G, cudaStream_t st);
 int group_allreduce_U(Group* G, Ctx* top, cudaStream_t st);
 
 // host-side precompute (api.cu)
-void make_line_coef(LineCoef* C, SchurInv* S, int64_t N, int L, double c, double a, double b, int mean_fix);
+void make_line_coef(LineCoef* C, SchurInv* S, int64_t N, int L, double c, double a, double b, int mean_fix,
+                    double* ext_host = nullptr);   // ext_host: 4 (L-1) doubles when L > kMaxL
 
 // launchers (fluid.cu)
 cudaError_t launch_s1_x(Ctx* s, int first_step);             // Steps 3a-3c: p*, momentum, x sweep

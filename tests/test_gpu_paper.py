@@ -67,7 +67,7 @@ def test_table5_thick_shell_rates_mu005():
     assert abs(r[1] - ref[1]) <= 0.15, (r, ref)
 
 
-@pytest.mark.parametrize("dim,n", [(2, 256), (2, 1024), (3, 64), (3, 128)])
+@pytest.mark.parametrize("dim,n", [(2, 256), (2, 1024), (2, 2048), (2, 4096), (3, 64), (3, 128)])
 def test_ds_solve_closed_form(dim, n):
     """§8(f2): A^{-1} f for the paper's single-mode f equals
     f / (1 + lam)^d, lam = 4 sin^2(pi h)/h^2, the exact discrete solution."""

@@ -40,7 +40,8 @@ def _gpu_for(pr, **kw):
 
 
 # ------------------------------------------------------------------ line solves
-@pytest.mark.parametrize("dim,n", [(2, 32), (2, 20), (2, 12), (2, 256), (2, 1024), (3, 16), (3, 20), (3, 128)])
+@pytest.mark.parametrize("dim,n", [(2, 32), (2, 20), (2, 12), (2, 256), (2, 1024), (2, 2048), (2, 4096), (3, 16),
+                                   (3, 20), (3, 128)])
 @pytest.mark.parametrize("which", ["visc", "psi"])
 def test_line_solve_parity(dim, n, which):
     """Batched cyclic solves along every axis vs the oracle's long-double
@@ -288,5 +289,21 @@ def test_cylinder_wrapped_fibres_ten_steps():
     fo, fg = o.fields(), g.fields()
     for c in range(3):
         assert _rel(fg["u"][c], fo["u"][c]) <= 1e-9 or np.abs(fo["u"][c]).max() < 1e-12, c
+    assert _rel(fg["p"], fo["p"]) <= 1e-9 and _rel(fg["X"], fo["X"]) <= 1e-9
+    g.close()
+
+
+@pytest.mark.parametrize("n", [2048, 4096])
+def test_large_2d_grids_five_steps(n):
+    """2D grids beyond 1024 (32 segments of 64 / 128 unknowns solved in shared memory):
+    the config-2 workload (4 ellipses) at N = 2048 / 4096, 5 steps against the oracle."""
+    from paper_1305_3976_b200 import inputs
+    pr = inputs.config(2, n=n, pts=2048)
+    o = _oracle_for(pr)
+    g = _gpu_for(pr)
+    o.step(5); g.step(5)
+    fo, fg = o.fields(), g.fields()
+    for c in range(2):
+        assert _rel(fg["u"][c], fo["u"][c]) <= 1e-9, c
     assert _rel(fg["p"], fo["p"]) <= 1e-9 and _rel(fg["X"], fo["X"]) <= 1e-9
     g.close()
