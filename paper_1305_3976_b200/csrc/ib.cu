@@ -48,6 +48,8 @@ __global__ void k_interp_evolve(const double* __restrict__ u0, const double* __r
                                 double* __restrict__ Uprev, double* __restrict__ Xold, double* __restrict__ Uold,
                                 int64_t npts, int n, double invh, double dt, int first)
 {
+    pdl_wait();
+    pdl_trigger();
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k >= npts) return;
     const double* uc[3] = {u0, u1, u2};
@@ -108,6 +110,8 @@ __global__ void k_force(const double* __restrict__ Xh, const int32_t* __restrict
                         const double* __restrict__ rest, int has_rest, double* __restrict__ F, int64_t npts,
                         double H, double invH)
 {
+    pdl_wait();
+    pdl_trigger();
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k >= npts) return;
     double xk[3] = {0, 0, 0}, acc[3] = {0, 0, 0};
@@ -844,6 +848,8 @@ __global__ void __launch_bounds__(256) k_spread_quad(const double* __restrict__ 
                                                      double* __restrict__ f2, int64_t npts, int n, double invh,
                                                      double invhd, double two_rho)
 {
+    pdl_wait();
+    pdl_trigger();
     const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 2;
     const int m0 = threadIdx.x & 3;
     const int64_t blk = g / (8 * DIM);
@@ -963,7 +969,7 @@ cudaError_t launch_interp_evolve(Ctx* s, int first)
     }
     const int thr = 128;
     const double invh = 1.0 / s->h;
-#define IBGM_IE(D, K) k_interp_evolve<D, K><<<nblk(s->npts, thr), thr, 0, s->stream>>>( \
+#define IBGM_IE(D, K) launch_pdl_if(D == 2, k_interp_evolve<D, K>, dim3(nblk(s->npts, thr)), dim3(thr), 0, s->stream, \
         s->u[0], s->u[1], s->u[2], s->X, s->Xh, s->Uprev, s->Xold, s->Uold, s->npts, (int)s->n, invh, s->dt, first)
     if (s->dim == 2) { if (s->kernel == IB_DELTA_COS4) IBGM_IE(2, 0); else IBGM_IE(2, 1); }
     else { if (s->kernel == IB_DELTA_COS4) IBGM_IE(3, 0); else IBGM_IE(3, 1); }
@@ -977,13 +983,11 @@ cudaError_t launch_force(Ctx* s)
     if (s->npts == 0) return cudaSuccess;
     const int thr = 128;
     if (s->dim == 2)
-        k_force<2><<<nblk(s->npts, thr), thr, 0, s->stream>>>(s->Xh, s->csr_ptr, s->csr_nbr, s->csr_kappa,
-                                                              s->csr_rest, s->has_rest, s->F, s->npts, s->H,
-                                                              1.0 / s->H);
+        launch_pdl_if(true, k_force<2>, dim3(nblk(s->npts, thr)), dim3(thr), 0, s->stream, s->Xh, s->csr_ptr, s->csr_nbr,
+                   s->csr_kappa, s->csr_rest, s->has_rest, s->F, s->npts, s->H, 1.0 / s->H);
     else
-        k_force<3><<<nblk(s->npts, thr), thr, 0, s->stream>>>(s->Xh, s->csr_ptr, s->csr_nbr, s->csr_kappa,
-                                                              s->csr_rest, s->has_rest, s->F, s->npts, s->H,
-                                                              1.0 / s->H);
+        launch_pdl_if(false, k_force<3>, dim3(nblk(s->npts, thr)), dim3(thr), 0, s->stream, s->Xh, s->csr_ptr, s->csr_nbr,
+                   s->csr_kappa, s->csr_rest, s->has_rest, s->F, s->npts, s->H, 1.0 / s->H);
     s->launches++;
     return cudaGetLastError();
 }
@@ -1086,8 +1090,9 @@ static cudaError_t launch_spread_quad(Ctx* s)
     const double invh = 1.0 / s->h;
     const double invhd = (s->dim == 3) ? invh * invh * invh : invh * invh;
     const double two_rho = 2.0 / s->rho;
-#define IBGM_SQ(D, K, KP) k_spread_quad<D, K, KP><<<nbk, 256, 0, s->stream>>>(s->Xh, s->F, s->wgt, s->nprev[0], \
-        s->nprev[1], s->nprev[2], s->f[0], s->f[1], s->f[2], s->npts, (int)s->n, invh, invhd, two_rho)
+#define IBGM_SQ(D, K, KP) launch_pdl_if(D == 2, k_spread_quad<D, K, KP>, dim3(nbk), dim3(256), 0, s->stream, s->Xh, s->F, \
+        s->wgt, s->nprev[0], s->nprev[1], s->nprev[2], s->f[0], s->f[1], s->f[2], s->npts, (int)s->n, invh, invhd, \
+        two_rho)
     const bool kp = s->debug_keep_f != 0;
     if (s->dim == 2) {
         if (s->kernel == IB_DELTA_COS4) { if (kp) IBGM_SQ(2, 0, true); else IBGM_SQ(2, 0, false); }

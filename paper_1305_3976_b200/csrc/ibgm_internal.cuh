@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "../../include/ibgm.h"
 
 namespace ibgm {
@@ -168,6 +170,42 @@ cudaError_t slab_spread_part(Ctx* top, Ctx* s, int* list, int* count);
 int group_halo(Group* G, int nf, const HaloSpec* spec, cudaStream_t st);
 int group_allgather(Group* G, cudaStream_t st);
 int group_allreduce_U(Group* G, Ctx* top, cudaStream_t st);
+
+// ---------------------------------------------------------------------------------
+// Programmatic dependent launch: a kernel launched with launch_pdl may become resident
+// while its predecessor in the stream drains; pdl_wait() (griddepcontrol.wait) blocks
+// until the predecessor has completed and its writes are visible, so it must precede
+// every read of data the predecessor produced.  pdl_trigger() lets the successor launch.
+// Without the launch attribute both are no-ops.
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl_if(bool on, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                 Args&&... args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = (on && pdl_enabled()) ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args)
+{
+    return launch_pdl_if(true, kern, grid, block, smem, st, std::forward<Args>(args)...);
+}
 
 // host-side precompute (api.cu)
 void make_line_coef(LineCoef* C, SchurInv* S, int64_t N, int L, double c, double a, double b, int mean_fix,
