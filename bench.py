@@ -128,6 +128,17 @@ def dist_env():
     return rank, world, local
 
 
+def arm_config(pr, cfg_idx, world):
+    """The `config` object of the JSON line (shared by both arms)."""
+    return {"workload": f"configs[{cfg_idx}]", "grid": f"{pr.n}^{pr.dim}", "ib_points": pr.npts,
+            "ib_edges": int(pr.edges.shape[0]) if pr.edges is not None else 0, "mu": pr.mu, "rho": pr.rho, "dt": pr.dt,
+            "delta_kernel": "cos4" if pr.kernel == 0 else "peskin4",
+            "parallelism": "single-gpu" if world == 1 else f"zslab{world}-nccl",
+            "l2": ("inputs larger than L2 (14 resident fp64 fields), no flush"
+                   if pr.ncell * 8 * (4 * pr.dim + 2) > 126e6 else
+                   "working set fits in L2 (no flush): a latency-bound parity config, not a roofline case")}
+
+
 def max_over_ranks(x: float) -> float:
     """Max of a per-rank scalar over all ranks (the slowest rank's time); identity
     without a process group.  Uses a CUDA tensor on NCCL, a CPU tensor on gloo."""
@@ -183,7 +194,7 @@ def run_reference(args):
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
            "steps": k, "warmup": 1, "ms_per_step": 1e3 * dt / k, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": f"configs[{args.config}]", "grid": f"{pr.n}^{pr.dim}", "ib_points": pr.npts},
+           "config": arm_config(pr, args.config, world),
            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
                             "sample": f"{k} of the requested {args.steps} oracle steps (bounded to ~{budget:.0f} s)"},
            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -304,10 +315,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": f"configs[{args.config}]", "grid": f"{n}^{dim}", "ib_points": pr.npts,
-                       "ib_edges": int(pr.edges.shape[0]), "mu": pr.mu, "rho": pr.rho, "dt": pr.dt,
-                       "delta_kernel": "cos4", "parallelism": "single-gpu" if world == 1 else f"zslab{world}-nccl",
-                       "l2": "inputs larger than L2 (17 resident fp64 fields), no flush"},
+            "config": arm_config(pr, args.config, world),
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "alg_bytes_per_launch": alg, "peak_source": peak_src,
