@@ -207,7 +207,9 @@ int ib_get_stats(ib_ctx* ctx, int64_t* kernel_launches, int64_t* steps_done);
  * select the interpolation: 0 automatic (= 1), 1 one thread per point, 2 box-staged,
  * 3 quad-lane.  The points are kept internally in Morton order of their initial
  * cells (outputs are returned in the caller's order).  Automatic by default.  Only
- * the single-GPU path honours bits 1-5. */
+ * the single-GPU path honours bits 1-5.  Set bit 0 before the first ib_step (or right
+ * after ib_set_fields): once the look-ahead has run the next step's IB phase, turning
+ * it on returns IB_ESTATE. */
 int ib_set_debug(ib_ctx* ctx, int32_t flags);
 
 /* Turn per-phase CUDA-event timing on (1) or off (0).  While on, ib_step records an

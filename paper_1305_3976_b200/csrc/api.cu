@@ -981,6 +981,8 @@ int ib_set_debug(ib_ctx* c, int32_t flags)
     if (!c) return fail(IB_EINVAL, "null context");
     Ctx* s = &c->s;
     const int keep = (flags & 1) != 0;
+    if (keep && !s->debug_keep_f && s->ib_ahead)
+        return fail(IB_ESTATE, "set debug bit 0 before stepping: the next step's IB phase has already run");
     for (int r = 0; r < nslabs(s); ++r) {
         Ctx* sl = slab_at(s, r);
         if (keep && !sl->f[0])

@@ -606,11 +606,10 @@ static cudaError_t go_lines_k(Ctx* s, int sys, const LArgs& la, int ncomp_grid, 
     auto kern = k_lines<L, KIND, DIM, AX, NC, MINB>;
     const int R = pick_r(s, L, tiles_of(KIND, NC));
     const size_t sm = lines_smem(s->P, L, tiles_of(KIND, NC), R);
-    static bool attr_set = false;   // per instantiation
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_limit());
+    static unsigned long long attr_mask = 0;   // per instantiation, per device
+    {
+        const cudaError_t e = smem_attr_once(attr_mask, kern, (int)smem_limit());
         if (e != cudaSuccess) return e;
-        attr_set = true;
     }
     dim3 grid((unsigned)((rows + R - 1) / R), (unsigned)gy, (unsigned)ncomp_grid);
     // PDL on 2D grids only: measured config 2 0.0896 -> 0.0846 ms/step; on 3D the waiting

@@ -927,11 +927,8 @@ static size_t spread_smem(int dim)
 template <int ID, class K>
 static cudaError_t box_attr(K kern, size_t sm)
 {
-    static bool done = false;
-    if (done) return cudaSuccess;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    if (e == cudaSuccess) done = true;
-    return e;
+    static unsigned long long mask = 0;   // per instantiation (ID), per device
+    return smem_attr_once(mask, kern, (int)sm);
 }
 
 cudaError_t launch_interp_evolve(Ctx* s, int first)
@@ -1007,11 +1004,10 @@ static cudaError_t go_brick_spread(Ctx* s)
 {
     auto kern = k_brick_spread<DIM, KER, B, KEEP>;
     const size_t sm = brick_smem(DIM, B);
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    static unsigned long long attr = 0;
+    {
+        const cudaError_t e = smem_attr_once(attr, kern, (int)sm);
         if (e != cudaSuccess) return e;
-        attr = true;
     }
     const double invh = 1.0 / s->h;
     const double invhd = (DIM == 3) ? invh * invh * invh : invh * invh;

@@ -183,6 +183,21 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 
 bool pdl_enabled();
 
+// Set a kernel's dynamic shared-memory limit once per device (function attributes are
+// per device): `mask` is the caller's static bitmask of devices already done.
+template <class K>
+inline cudaError_t smem_attr_once(unsigned long long& mask, K kern, int bytes)
+{
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (mask & bit) return cudaSuccess;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) mask |= bit;
+    return e;
+}
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl_if(bool on, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                                  Args&&... args)
