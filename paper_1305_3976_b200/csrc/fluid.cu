@@ -317,105 +317,6 @@ __device__ __forceinline__ void s1_cell(const S1Args& A, int i, const RowB& rb, 
     }
 }
 
-// The same cell with the x-shifted operands taken from neighbouring lanes: when a warp
-// covers 32 consecutive x of one row (n % 32 == 0), u(I +- e_x), the four mixed skew
-// terms shifted along x and p*(I - e_x) are shuffles of values the neighbour lanes
-// loaded; only the warp-edge lanes load them (a row of exactly 32 wraps inside the
-// warp).  23 global loads per cell instead of 34; same arithmetic as s1_cell.
-#ifndef IBGM_S1_SHFL
-#define IBGM_S1_SHFL 1
-#endif
-// lanes of a warp hold 32 consecutive x of one row iff n % 32 == 0 (both fill paths).
-// Used for 2D only: measured config 2 S1 38.3 -> 35.1 us, but config 3 68 -> 97 us.
-__device__ __forceinline__ bool s1_shfl_on(int n) { return IBGM_S1_SHFL && (n & 31) == 0; }
-
-template <int DIM>
-__device__ __forceinline__ void s1_cell_shfl(const S1Args& A, int i, const RowB& rb, int n, double (&d)[3])
-{
-    const int lane = threadIdx.x & 31;
-    const bool wrap32 = (n == 32);
-    const bool lo_edge = (lane == 0) && !wrap32, hi_edge = (lane == 31) && !wrap32;
-    const int im = (i == 0) ? n - 1 : i - 1, ip = (i == n - 1) ? 0 : i + 1, ii = i;
-    const int srcm = (lane + 31) & 31, srcp = (lane + 1) & 31;
-    // per component: I, I+e_y, I-e_y, I+e_z, I-e_z (coalesced rows)
-    double C0[3], Cyp[3], Cym[3], Czp[3], Czm[3], Cxp[3], Cxm[3];
-#pragma unroll
-    for (int m = 0; m < DIM; ++m) {
-        const double* um = A.u[m];
-        C0[m] = ldg(um + ii + rb.r0);
-        Cyp[m] = ldg(um + ii + rb.ryp);
-        Cym[m] = ldg(um + ii + rb.rym);
-        if (DIM == 3) {
-            Czp[m] = ldg(um + ii + rb.rzp);
-            Czm[m] = ldg(um + ii + rb.rzm);
-        }
-    }
-#pragma unroll
-    for (int m = 0; m < DIM; ++m) {
-        Cxp[m] = __shfl_sync(kFull, C0[m], srcp);
-        Cxm[m] = __shfl_sync(kFull, C0[m], srcm);
-        if (hi_edge) Cxp[m] = ldg(A.u[m] + ip + rb.r0);
-        if (lo_edge) Cxm[m] = ldg(A.u[m] + im + rb.r0);
-    }
-    // mixed terms u_m(I + e_m - e_c), m != c
-    double X[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
-    if (A.advection) {
-        // x-shifted: from the lane holding i+1 / i-1
-        X[0][1] = __shfl_sync(kFull, Cym[0], srcp);            // u_x(i+1, j-1)
-        X[1][0] = __shfl_sync(kFull, Cyp[1], srcm);            // u_y(i-1, j+1)
-        if (hi_edge) X[0][1] = ldg(A.u[0] + ip + rb.rym);
-        if (lo_edge) X[1][0] = ldg(A.u[1] + im + rb.ryp);
-        if (DIM == 3) {
-            X[0][2] = __shfl_sync(kFull, Czm[0], srcp);        // u_x(i+1, k-1)
-            X[2][0] = __shfl_sync(kFull, Czp[2], srcm);        // u_z(i-1, k+1)
-            if (hi_edge) X[0][2] = ldg(A.u[0] + ip + rb.rzm);
-            if (lo_edge) X[2][0] = ldg(A.u[2] + im + rb.rzp);
-            X[1][2] = ldg(A.u[1] + ii + rb.rypzm);             // u_y(j+1, k-1)
-            X[2][1] = ldg(A.u[2] + ii + rb.rymzp);             // u_z(j-1, k+1)
-        }
-    }
-    double ps0 = 0.0, psm[3] = {0, 0, 0};
-    if (!A.first) {
-        ps0 = ldg(A.pstar + ii + rb.r0);
-        psm[1] = ldg(A.pstar + ii + rb.rym);
-        if (DIM == 3) psm[2] = ldg(A.pstar + ii + rb.rzm);
-    }
-    {
-        const double t0 = __shfl_sync(kFull, ps0, srcm);
-        psm[0] = (lo_edge && !A.first) ? ldg(A.pstar + im + rb.r0) : t0;
-    }
-    const double invh = A.invh;
-    const double dt_rho = A.dt * A.inv_rho;
-#pragma unroll
-    for (int c = 0; c < DIM; ++c) {
-        const double u0 = C0[c];
-        // u_c(I + e_j), u_c(I - e_j)
-        const double upj[3] = {Cxp[c], Cyp[c], (DIM == 3) ? Czp[c] : 0.0};
-        const double umj[3] = {Cxm[c], Cym[c], (DIM == 3) ? Czm[c] : 0.0};
-        double Nc = 0.0;
-        if (A.advection) {
-#pragma unroll
-            for (int jd = 0; jd < DIM; ++jd) {
-                // u_j(I + e_j) and u_j(I - e_c)
-                const double ujp = (jd == 0) ? Cxp[0] : (jd == 1 ? Cyp[1] : Czp[2]);
-                const double ujm = (c == 0) ? Cxm[jd] : (c == 1 ? Cym[jd] : Czm[jd]);
-                const double Tp = ujp + ((jd == c) ? u0 : X[jd][c]);
-                const double Tm = C0[jd] + ujm;
-                Nc = fma(Tp, upj[jd], Nc);
-                Nc = fma(-Tm, umj[jd], Nc);
-            }
-            Nc *= 0.25 * invh;
-        }
-        A.nadv[c][ii + rb.r0] = Nc;
-        double lap = Cxp[c] + Cxm[c] + Cyp[c] + Cym[c];
-        if (DIM == 3) lap += Czp[c] + Czm[c];
-        lap = (lap - 2.0 * DIM * u0) * (invh * invh);
-        const double gp = A.first ? 0.0 : (ps0 - psm[c]) * invh;
-        const double Gc = ldg(A.G[c] + ii + rb.r0);
-        d[c] = A.dt * (0.5 * Gc - A.a1 * Nc) + dt_rho * (A.mu * lap - gp);
-    }
-}
-
 // -------------------------------------------------------------------------------
 // The line-pass kernel.  AX: line axis (0 = x, rows of R consecutive j at fixed k;
 // 1 = y / 2 = z, R consecutive i at fixed k / j).  NC tiles are staged (NC = DIM for
@@ -482,8 +383,7 @@ struct LinePass {
                     const RowB rb = row_bases<DIM>(g0 + l, (int)tb, n, A.nl, A.wrap);
                     for (int m = t; m < n; m += T) {
                         double v[3];
-                        if (DIM == 2 && s1_shfl_on(n)) s1_cell_shfl<DIM>(A.s1, m, rb, n, v);
-                        else s1_cell<DIM>(A.s1, m, rb, n, v);
+                        s1_cell<DIM>(A.s1, m, rb, n, v);
                         const int off = tile_off<L>(l, m, TP);
 #pragma unroll
                         for (int c = 0; c < NC; ++c) tile[c * RTP + off] = v[c];
@@ -496,8 +396,7 @@ struct LinePass {
                     for (int l = l0; l < R && g0 + l < nrow; l += rows) {
                         const RowB rb = row_bases<DIM>(g0 + l, (int)tb, n, A.nl, A.wrap);
                         double v[3];
-                        if (DIM == 2 && s1_shfl_on(n)) s1_cell_shfl<DIM>(A.s1, m, rb, n, v);
-                        else s1_cell<DIM>(A.s1, m, rb, n, v);
+                        s1_cell<DIM>(A.s1, m, rb, n, v);
                         const int off = tile_off<L>(l, m, TP);
 #pragma unroll
                         for (int c = 0; c < NC; ++c) tile[c * RTP + off] = v[c];
