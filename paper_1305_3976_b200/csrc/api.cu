@@ -508,6 +508,8 @@ int ib_create(const ib_grid* grid, double nu, double rho, double dt, const ib_op
             while (G->Q < nz && nz % G->Q != 0) ++G->Q;
             if ((int64_t)s->plane * G->Q >= 65536) break;
         }
+        // parts of at most 33 planes, so the forward phase keeps its column in registers
+        while (nz / G->Q > 33 || nz % G->Q != 0) ++G->Q;
         if (nz / G->Q < 2) G->Q = nz / 2;
         if (G->Q * P > 128) G->Q = 128 / P > 0 ? 128 / P : 1;   // the reduced system stays <= 128 parts
         if (G->Q < 1) G->Q = 1;
