@@ -250,6 +250,29 @@ __device__ __forceinline__ RowB row_bases(int j, int k, int n, int nl, int wrap)
 // (1/2)[ sum_j (TA|+ - TA|-)/h + sum_j (Tg|- + Tg|+)/2 ] collapses exactly (the u_c(I)
 // terms cancel) to
 //   N_c = 1/(4h) sum_j [ (u_j(I+e_j) + u_j(I+e_j-e_c)) u_c(I+e_j) - (u_j(I) + u_j(I-e_c)) u_c(I-e_j) ]
+// L2 prefetch of the operands that miss in L1/L2 for cell i of a row (its centre, its
+// z-neighbour planes, the history G and p*), issued one row ahead by the fill loop
+#ifndef IBGM_S1_PREFETCH
+#define IBGM_S1_PREFETCH 1
+#endif
+__device__ __forceinline__ void pf_l2(const double* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
+template <int DIM>
+__device__ __forceinline__ void s1_prefetch(const S1Args& A, int i, const RowB& rb)
+{
+    if (!IBGM_S1_PREFETCH) return;
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) {
+        pf_l2(A.u[c] + i + rb.r0);
+        if (DIM == 3) {
+            pf_l2(A.u[c] + i + rb.rzp);
+            pf_l2(A.u[c] + i + rb.rzm);
+        }
+        pf_l2(A.G[c] + i + rb.r0);
+    }
+    pf_l2(A.pstar + i + rb.r0);
+}
+
 template <int DIM>
 __device__ __forceinline__ void s1_cell(const S1Args& A, int i, const RowB& rb, int n, double (&d)[3])
 {
@@ -379,8 +402,12 @@ struct LinePass {
         const int nrow = (DIM == 2) ? A.nl : n;
         if (KIND == K_S1) {
             if (n >= T) {
-                for (int l = 0; l < R && g0 + l < nrow; ++l) {
+                    for (int l = 0; l < R && g0 + l < nrow; ++l) {
                     const RowB rb = row_bases<DIM>(g0 + l, (int)tb, n, A.nl, A.wrap);
+                    if (l + 1 < R && g0 + l + 1 < nrow) {
+                        const RowB rn = row_bases<DIM>(g0 + l + 1, (int)tb, n, A.nl, A.wrap);
+                        for (int m = t; m < n; m += T) s1_prefetch<DIM>(A.s1, m, rn);
+                    }
                     for (int m = t; m < n; m += T) {
                         double v[3];
                         s1_cell<DIM>(A.s1, m, rb, n, v);
@@ -395,6 +422,8 @@ struct LinePass {
                 if (l0 < rows)
                     for (int l = l0; l < R && g0 + l < nrow; l += rows) {
                         const RowB rb = row_bases<DIM>(g0 + l, (int)tb, n, A.nl, A.wrap);
+                        if (l + rows < R && g0 + l + rows < nrow)
+                            s1_prefetch<DIM>(A.s1, m, row_bases<DIM>(g0 + l + rows, (int)tb, n, A.nl, A.wrap));
                         double v[3];
                         s1_cell<DIM>(A.s1, m, rb, n, v);
                         const int off = tile_off<L>(l, m, TP);
