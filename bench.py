@@ -76,13 +76,17 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), "--query-gpu=" + ",".join(self.FIELDS),
-                 "--format=csv,noheader,nounits", "-lms", "50"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except Exception:  # noqa: BLE001
             self.proc = None
-        time.sleep(0.15)
+        # the timed region must not start before nvidia-smi is actually sampling
+        t0 = time.time()
+        while self.proc is not None and not self.lines and time.time() - t0 < 10.0:
+            time.sleep(0.02)
+        self.n0 = len(self.lines)
         return self
 
     def _read(self):
@@ -99,8 +103,8 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm, smax, reasons, util = [], [], set(), []
-        for l in self.lines:
+        sm, smax, reasons, util, allsm = [], [], set(), [], []
+        for l in self.lines[getattr(self, "n0", 0):]:     # samples taken during the timed region
             parts = [x.strip() for x in l.split(",")]
             if len(parts) < len(self.FIELDS):
                 continue
@@ -110,15 +114,19 @@ class ClockSampler:
                 continue
             u = float(parts[6]) if parts[6].replace(".", "").isdigit() else 0.0
             util.append(u)
+            allsm.append(s)
             if u > 0:
                 sm.append(s)
             smax.append(m)
             for nm, v in zip(self.NAMES, parts[2:6]):
                 if v.lower() == "active":
                     reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None,
+        # utilization.gpu is a trailing average and can read 0 in a short region: then
+        # every sample of the region counts
+        use = sm if sm else allsm
+        return {"sm_mhz": statistics.median(use) if use else None,
                 "sm_max_mhz": max(smax) if smax else None,
-                "reasons": sorted(reasons), "samples": len(self.lines), "samples_under_load": len(sm)}
+                "reasons": sorted(reasons), "samples": len(allsm), "samples_under_load": len(sm)}
 
 
 def dist_env():
