@@ -255,7 +255,17 @@ __device__ __forceinline__ RowB row_bases(int j, int k, int n, int nl, int wrap)
 #ifndef IBGM_S1_PREFETCH
 #define IBGM_S1_PREFETCH 1
 #endif
-__device__ __forceinline__ void pf_l2(const double* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+#ifndef IBGM_PF_L1
+#define IBGM_PF_L1 0
+#endif
+#ifndef IBGM_PF_DIST
+#define IBGM_PF_DIST 2
+#endif
+__device__ __forceinline__ void pf_l2(const double* p)
+{
+    if (IBGM_PF_L1) asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+    else asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
 
 template <int DIM>
 __device__ __forceinline__ void s1_prefetch(const S1Args& A, int i, const RowB& rb)
@@ -422,8 +432,9 @@ struct LinePass {
                 if (l0 < rows)
                     for (int l = l0; l < R && g0 + l < nrow; l += rows) {
                         const RowB rb = row_bases<DIM>(g0 + l, (int)tb, n, A.nl, A.wrap);
-                        if (l + rows < R && g0 + l + rows < nrow)
-                            s1_prefetch<DIM>(A.s1, m, row_bases<DIM>(g0 + l + rows, (int)tb, n, A.nl, A.wrap));
+                        if (l + IBGM_PF_DIST * rows < R && g0 + l + IBGM_PF_DIST * rows < nrow)
+                            s1_prefetch<DIM>(A.s1, m,
+                                             row_bases<DIM>(g0 + l + IBGM_PF_DIST * rows, (int)tb, n, A.nl, A.wrap));
                         double v[3];
                         s1_cell<DIM>(A.s1, m, rb, n, v);
                         const int off = tile_off<L>(l, m, TP);
