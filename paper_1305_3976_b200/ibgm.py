@@ -174,9 +174,11 @@ class Context:
         return (self.nz,) + (self.n,) * (self.dim - 1)
 
     def close(self):
-        if getattr(self, "_h", None):
-            lib().ib_destroy(self._h)
-            self._h = None
+        h = getattr(self, "_h", None)
+        self._h = None
+        L = _lib   # module globals may already be torn down at interpreter exit
+        if h and L is not None:
+            L.ib_destroy(h)
 
     def __del__(self):
         self.close()
