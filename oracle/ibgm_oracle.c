@@ -7,8 +7,9 @@
  * PAPER.md passage it follows ("PAPER.md:L" = line L of the paper's LaTeX source).
  *
  * Rules (DESIGN.md section "Oracle"):
- *   - Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg may
- *     load this library.  The product path (paper_1305_3976_b200/) never does.
+ *   - Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg (and its
+ *     --impl reference arm) may load this library.  The product path
+ *     (paper_1305_3976_b200/) never does.
  *   - It shares no code, header, table or constant generator with the CUDA path.
  *   - fp64 fields; the cyclic tridiagonal line solves run in long double
  *     (SURVEY A16 reading, R16); compiled with -ffp-contract=off.
@@ -21,7 +22,11 @@
  *             stencils (eigenvalues / identities), skew advection (energy
  *             identity + 2nd-order convergence), cyclic solves (dense LU),
  *             viscous Douglas sweeps (Stokes Taylor-Green closed form),
- *             psi / p pipeline (per-Fourier-mode linear recurrence), start-up.
+ *             psi / p pipeline (per-Fourier-mode linear recurrence), start-up,
+ *             minimum-image force connections (R26: through-the-boundary spring
+ *             equals its nearby image), box side H (R2: the 2x2 ellipse array on
+ *             [0,2]^2 equals the tiled single ellipse), and the whole method against
+ *             the paper's Table 6.
  *   parity unpinned: the choice of the cosine kernel (COS4) for the BASELINE
  *             configs, the 3D edge-spring scaling (kappa=sigma, w=1) and the
  *             input sampling recipes -- these are BASELINE-defined, not paper-defined.
