@@ -508,8 +508,8 @@ int ib_create(const ib_grid* grid, double nu, double rho, double dt, const ib_op
             while (G->Q < nz && nz % G->Q != 0) ++G->Q;
             if ((int64_t)s->plane * G->Q >= 65536) break;
         }
-        // parts of at most 33 planes, so the forward phase keeps its column in registers
-        while (nz / G->Q > 33 || nz % G->Q != 0) ++G->Q;
+        // (Q stays 1 when one part per slab already gives enough threads: every extra
+        //  part adds one reduced-system row per line to the all-gather)
         if (nz / G->Q < 2) G->Q = nz / 2;
         if (G->Q * P > 128) G->Q = 128 / P > 0 ? 128 / P : 1;   // the reduced system stays <= 128 parts
         if (G->Q < 1) G->Q = 1;
@@ -942,7 +942,7 @@ static int enqueue_step_slab(Ctx* s, int first)
     // the last Douglas sweep along the cut axis (distributed Schur solve)
     if (s->profiling) CKC(cudaEventRecord(s->ev[last_ph][0], s->stream));
     FOR_SLABS(slab_sweep_last_fwd(sl, G));
-    CKG(group_allgather(G, s->stream));
+    CKG(group_allgather(G, 2 * d, s->stream));
     FOR_SLABS(slab_sweep_last_corr(sl, G));
     if (s->profiling) {
         CKC(cudaEventRecord(s->ev[last_ph][1], s->stream));
@@ -955,7 +955,7 @@ static int enqueue_step_slab(Ctx* s, int first)
         CKG(group_halo(G, 1, h, s->stream));
     }
     FOR_SLABS(slab_divpsi_fwd(sl, G));
-    CKG(group_allgather(G, s->stream));
+    CKG(group_allgather(G, 4, s->stream));
     FOR_SLABS(slab_divpsi_corr(sl, G));
     if (s->profiling) {
         CKC(cudaEventRecord(s->ev[IB_PH_DIVPSI][1], s->stream));
@@ -1094,7 +1094,7 @@ int ib_line_solve(ib_ctx* c, int32_t axis, double kappa, const double* d, double
                                 cudaMemcpyHostToDevice, s->stream));
         }
         FOR_SLABS(slab_user_fwd(sl, s->grp, sl->tmp, mf));
-        CKG(group_allgather(s->grp, s->stream));
+        CKG(group_allgather(s->grp, mf ? 4 : 2, s->stream));
         FOR_SLABS(slab_user_corr(sl, s->grp, sl->tmp, mf));
         for (int r = 0; r < nslabs(s); ++r) {
             Ctx* sl = slab_at(s, r);

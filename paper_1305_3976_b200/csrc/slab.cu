@@ -127,6 +127,7 @@ struct SlabArgs {
     double neg_rho_dt, chimu_half, invh;
     int n, nz, rank;
     int Q, Lseg;              // Schur parts per slab and their length (nz = Q Lseg)
+    int ns;                   // gather slots per part of this solve (6 viscous: 2 per component; 4 psi)
     long long plane;          // N^{d-1}
 };
 
@@ -194,7 +195,7 @@ __global__ void __launch_bounds__(128) k_slab_fwd(SlabCf C, SlabArgs A, int slot
         io[i * PL + q] = x;
         fsum += x;
     }
-    double* g = A.gather + ((long long)part * kSlabSlots + slot0 + 2 * comp) * PL;
+    double* g = A.gather + ((long long)part * A.ns + slot0 + 2 * comp) * PL;
     g[q] = d0 - b * x;                  // x = f*_1 here
     g[PL + q] = fm;
     if (MF) {
@@ -276,7 +277,7 @@ __global__ void __launch_bounds__(128) k_slab_fwd_reg(SlabCf C, SlabArgs A, int 
             io[i * PL + q] = d[i];
             fsum += d[i];
         }
-    double* g = A.gather + ((long long)part * kSlabSlots + slot0 + 2 * comp) * PL;
+    double* g = A.gather + ((long long)part * A.ns + slot0 + 2 * comp) * PL;
     g[q] = d[0] - b * d[1];
     g[PL + q] = fm;
     if (MF) {
@@ -308,8 +309,8 @@ __global__ void __launch_bounds__(128) k_slab_corr(SlabCf C, SlabArgs A, int slo
     double ys = 0.0, ys1 = 0.0, ysum = 0.0, D = 0.0, F = 0.0;
     for (int t = 0; t < P; ++t) {
         const int tp = (t == 0) ? P - 1 : t - 1;
-        const double* gt = A.gather + ((long long)t * kSlabSlots + slot0) * PL;
-        const double* gp = A.gather + ((long long)tp * kSlabSlots + slot0) * PL;
+        const double* gt = A.gather + ((long long)t * A.ns + slot0) * PL;
+        const double* gp = A.gather + ((long long)tp * A.ns + slot0) * PL;
         const double r = gt[q] - c * gp[PL + q];
         ys = fma(SI[s * P + t], r, ys);
         ys1 = fma(SI[s1 * P + t], r, ys1);
@@ -380,6 +381,7 @@ static SlabArgs slab_args(Ctx* s, Group* G)
 cudaError_t slab_sweep_last_fwd(Ctx* s, Group* G)
 {
     SlabArgs a = slab_args(s, G);
+    a.ns = 2 * s->dim;
     for (int c = 0; c < s->dim; ++c) { a.io[c] = s->st[c]; a.un[c] = s->u[c]; }
     SlabCf C{G->coef[SYS_VISC], (int)(s->nl / G->Q) - 1, G->P * G->Q};
     if (s->dim == 3) return launch_fwd<3, SRC_FIELD, 0>(s, C, a, 3);
@@ -389,6 +391,7 @@ cudaError_t slab_sweep_last_fwd(Ctx* s, Group* G)
 cudaError_t slab_sweep_last_corr(Ctx* s, Group* G)
 {
     SlabArgs a = slab_args(s, G);
+    a.ns = 2 * s->dim;
     for (int c = 0; c < s->dim; ++c) { a.io[c] = s->st[c]; a.un[c] = s->u[c]; }
     SlabCf C{G->coef[SYS_VISC], (int)(s->nl / G->Q) - 1, G->P * G->Q};
     k_slab_corr<EPI_ADD_UN, 0><<<dim3(nb128(s->plane), (unsigned)s->dim, (unsigned)a.Q), 128, 0, s->stream>>>(C, a, 0);
@@ -400,6 +403,7 @@ cudaError_t slab_sweep_last_corr(Ctx* s, Group* G)
 cudaError_t slab_divpsi_fwd(Ctx* s, Group* G)
 {
     SlabArgs a = slab_args(s, G);
+    a.ns = 4;
     a.io[0] = a.io[1] = a.io[2] = s->pstar;
     for (int c = 0; c < s->dim; ++c) { a.un[c] = s->u[c]; a.unew[c] = s->st[c]; }
     a.p = s->p;
@@ -411,6 +415,7 @@ cudaError_t slab_divpsi_fwd(Ctx* s, Group* G)
 cudaError_t slab_divpsi_corr(Ctx* s, Group* G)
 {
     SlabArgs a = slab_args(s, G);
+    a.ns = 4;
     a.io[0] = a.io[1] = a.io[2] = s->pstar;
     SlabCf C{G->coef[SYS_PSI], (int)(s->nl / G->Q) - 1, G->P * G->Q};
     k_slab_corr<EPI_STORE, 1><<<dim3(nb128(s->plane), 1, (unsigned)a.Q), 128, 0, s->stream>>>(C, a, 0);
@@ -422,6 +427,7 @@ cudaError_t slab_divpsi_corr(Ctx* s, Group* G)
 cudaError_t slab_user_fwd(Ctx* s, Group* G, double* data, int mf)
 {
     SlabArgs a = slab_args(s, G);
+    a.ns = mf ? 4 : 2;
     a.io[0] = a.io[1] = a.io[2] = data;
     SlabCf C{G->coef[SYS_USER], (int)(s->nl / G->Q) - 1, G->P * G->Q};
     if (mf) {
@@ -435,6 +441,7 @@ cudaError_t slab_user_fwd(Ctx* s, Group* G, double* data, int mf)
 cudaError_t slab_user_corr(Ctx* s, Group* G, double* data, int mf)
 {
     SlabArgs a = slab_args(s, G);
+    a.ns = mf ? 4 : 2;
     a.io[0] = a.io[1] = a.io[2] = data;
     SlabCf C{G->coef[SYS_USER], (int)(s->nl / G->Q) - 1, G->P * G->Q};
     const dim3 grid(nb128(s->plane), 1, (unsigned)a.Q);
@@ -757,10 +764,10 @@ int group_halo(Group* G, int nf, const HaloSpec* spec, cudaStream_t st)
 }
 
 // every rank's reduced-system scalars to every rank (EMULATE: the buffer is shared)
-int group_allgather(Group* G, cudaStream_t st)
+int group_allgather(Group* G, int ns, cudaStream_t st)
 {
     if (G->transport == IB_TRANSPORT_EMULATE) return 0;
-    const size_t cnt = (size_t)G->Q * kSlabSlots * G->slab[0]->plane;   // this rank's Q parts
+    const size_t cnt = (size_t)G->Q * ns * G->slab[0]->plane;   // this rank's Q parts, ns slots each
     return g_nccl.AllGather(G->gather + (size_t)G->rank * cnt, G->gather, cnt, kNcclDouble, G->comm, st);
 }
 
