@@ -509,14 +509,27 @@ int ib_create(const ib_grid* grid, double nu, double rho, double dt, const ib_op
             if ((int64_t)s->plane * G->Q >= 65536) break;
         }
         // (Q stays 1 when one part per slab already gives enough threads: every extra
-        //  part adds one reduced-system row per line to the all-gather)
+        //  part adds one reduced-system row per line to the master exchange)
         if (nz / G->Q < 2) G->Q = nz / 2;
-        if (G->Q * P > 128) G->Q = 128 / P > 0 ? 128 / P : 1;   // the reduced system stays <= 128 parts
+        if (G->Q * P > kSlabMaxParts) G->Q = kSlabMaxParts / P > 0 ? kSlabMaxParts / P : 1;   // reduced system <= kSlabMaxParts
         if (G->Q < 1) G->Q = 1;
         while (nz % G->Q != 0) --G->Q;
-        const size_t gsz = sizeof(double) * (size_t)P * G->Q * kSlabSlots * s->plane;
-        CKC(cudaMalloc(&G->gather, gsz));
-        CKC(cudaMemsetAsync(G->gather, 0, gsz, s->stream));
+        {
+            // exchange buffers (slab.cu): EMULATE keeps one shared UP / DN, NCCL a send and
+            // a receive buffer each
+            const size_t NI = (size_t)(s->plane / P), nb = (size_t)G->Q + 2;
+            const bool emu = (o.transport == IB_TRANSPORT_EMULATE);
+            const size_t up = (size_t)P * G->Q * kSlabSlots * NI * (emu ? P : 1);
+            const size_t dn = (size_t)P * 3 * nb * NI * (emu ? P : 1);
+            CKC(cudaMalloc(&G->up_s, up * sizeof(double)));
+            CKC(cudaMalloc(&G->dn_s, dn * sizeof(double)));
+            CKC(cudaMemsetAsync(G->up_s, 0, up * sizeof(double), s->stream));
+            CKC(cudaMemsetAsync(G->dn_s, 0, dn * sizeof(double), s->stream));
+            if (!emu) {
+                CKC(cudaMalloc(&G->up_rv, up * sizeof(double)));
+                CKC(cudaMalloc(&G->dn_rv, dn * sizeof(double)));
+            }
+        }
         int rc;
         if ((rc = upload_coef(s, SYS_VISC, -kv, 1.0 + 2.0 * kv, -kv, 0)) != IB_OK) return rc;
         if ((rc = upload_coef(s, SYS_PSI, -kp, 1.0 + 2.0 * kp, -kp, 1)) != IB_OK) return rc;
@@ -942,7 +955,9 @@ static int enqueue_step_slab(Ctx* s, int first)
     // the last Douglas sweep along the cut axis (distributed Schur solve)
     if (s->profiling) CKC(cudaEventRecord(s->ev[last_ph][0], s->stream));
     FOR_SLABS(slab_sweep_last_fwd(sl, G));
-    CKG(group_allgather(G, 2 * d, s->stream));
+    CKG(group_up(G, 2 * d, s->stream));
+    CKC(slab_master(G->slab[0], G, SYS_VISC, d, 2 * d, 0));
+    CKG(group_dn(G, d, s->stream));
     FOR_SLABS(slab_sweep_last_corr(sl, G));
     if (s->profiling) {
         CKC(cudaEventRecord(s->ev[last_ph][1], s->stream));
@@ -955,7 +970,9 @@ static int enqueue_step_slab(Ctx* s, int first)
         CKG(group_halo(G, 1, h, s->stream));
     }
     FOR_SLABS(slab_divpsi_fwd(sl, G));
-    CKG(group_allgather(G, 4, s->stream));
+    CKG(group_up(G, 4, s->stream));
+    CKC(slab_master(G->slab[0], G, SYS_PSI, 1, 4, 1));
+    CKG(group_dn(G, 1, s->stream));
     FOR_SLABS(slab_divpsi_corr(sl, G));
     if (s->profiling) {
         CKC(cudaEventRecord(s->ev[IB_PH_DIVPSI][1], s->stream));
@@ -1094,7 +1111,9 @@ int ib_line_solve(ib_ctx* c, int32_t axis, double kappa, const double* d, double
                                 cudaMemcpyHostToDevice, s->stream));
         }
         FOR_SLABS(slab_user_fwd(sl, s->grp, sl->tmp, mf));
-        CKG(group_allgather(s->grp, mf ? 4 : 2, s->stream));
+        CKG(group_up(s->grp, mf ? 4 : 2, s->stream));
+        CKC(slab_master(s->grp->slab[0], s->grp, SYS_USER, 1, mf ? 4 : 2, mf));
+        CKG(group_dn(s->grp, 1, s->stream));
         FOR_SLABS(slab_user_corr(sl, s->grp, sl->tmp, mf));
         for (int r = 0; r < nslabs(s); ++r) {
             Ctx* sl = slab_at(s, r);
@@ -1203,7 +1222,7 @@ int ib_destroy(ib_ctx* c)
             free_fields(G->slab[r]);
             delete G->slab[r];
         }
-        cudaFree(G->gather);
+        cudaFree(G->up_s); cudaFree(G->up_rv); cudaFree(G->dn_s); cudaFree(G->dn_rv);
         for (int k = 0; k < SYS_COUNT; ++k) cudaFree(G->coef[k]);
         free_lagrangian(s);
         nccl_comm_destroy(G->comm);

@@ -126,6 +126,7 @@ struct NcclUid { char internal[128]; };
 // slab coefficient block header (doubles), followed by inv, cp, g, h [m], S^{-1} [P*P],
 // colsum(S^{-1}) [P]
 enum { SC_C = 0, SC_A, SC_B, SC_INVROW, SC_GSUM, SC_HSUM, SC_N, SC_MF, SC_HDR = 8 };
+constexpr int kSlabMaxParts = 128;  // parts of the cut-axis reduced system (P Q), k_slab_master
 constexpr int kSlabSlots = 6;         // max gather slots per part: 2 per velocity component / 4 for psi
 constexpr int kMaxRanks = 64;
 
@@ -136,7 +137,8 @@ struct Group {
     int nloc;                         // slabs held by this context (P emulated, 1 with NCCL)
     int Q;                            // Schur parts per slab along the cut axis (nz = Q Lseg)
     Ctx* slab[kMaxRanks];
-    double* gather;                   // [P Q][ns][plane], ns <= kSlabSlots per solve
+    double *up_s, *up_rv;             // reduced-system scalars to the line masters (slab.cu layouts)
+    double *dn_s, *dn_rv;             // y values and corrections back from the masters
     double* Upart;                    // partial interpolation ([P][npts*d] emulated, [npts*d] NCCL)
     double* Ured;                     // U^n after the sum over ranks
     int64_t ucap;                     // capacity (points*d) of Upart/Ured
@@ -168,7 +170,9 @@ cudaError_t slab_sum_slots(Ctx* top, const double* part, int P, double* out);
 cudaError_t slab_evolve(Ctx* top, const double* U, int first);
 cudaError_t slab_spread_part(Ctx* top, Ctx* s, int* list, int* count);
 int group_halo(Group* G, int nf, const HaloSpec* spec, cudaStream_t st);
-int group_allgather(Group* G, int ns, cudaStream_t st);   // ns slots per part
+int group_up(Group* G, int ns, cudaStream_t st);          // scalars to the line masters
+int group_dn(Group* G, int ncomp, cudaStream_t st);       // y and corrections back
+cudaError_t slab_master(Ctx* s, Group* G, int sys, int ncomp, int ns, int mf);
 int group_allreduce_U(Group* G, Ctx* top, cudaStream_t st);
 
 // ---------------------------------------------------------------------------------

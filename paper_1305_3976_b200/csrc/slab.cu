@@ -14,17 +14,18 @@
 // ranks: slab s is part s of every line -- its first plane is the
 // interface unknown y_s and planes 1..nz-1 are the interior block B_s.  Each rank
 // solves B_s f*_s = d_s (Thomas, one thread per line, coalesced across x), publishes
-// per line the scalars the reduced system needs, an all-gather replaces the paper's
-// gather to the master rank (every rank then holds the whole reduced right-hand side),
-// and each rank applies the precomputed S^{-1} to get its own y_s, y_{s+1} and
-// corrects x_s = f*_s - B_s^{-1} E_s y.
+// per line the scalars the reduced system needs to that line's master rank (line index
+// mod P, as in the paper's PAPER.md:1270-1276), the master applies the precomputed
+// S^{-1} and sends each rank back only its y_s, y_{s+1} and the line-mean correction,
+// and each rank corrects x_s = f*_s - B_s^{-1} E_s y.
 //
 // Two transports move the halo planes, the reduced system and the partial U:
-//   EMULATE  P virtual slabs in one context on one GPU (device-to-device copies and a
-//            shared gather buffer) -- the same kernels in the same order, used to test
-//            the decomposition at the parity bar with a single GPU;
+//   EMULATE  P virtual slabs in one context on one GPU (device-to-device copies and
+//            shared exchange buffers) -- the same kernels in the same order, used to
+//            test the decomposition at the parity bar with a single GPU;
 //   NCCL     one slab per process (one process per GPU), grouped ncclSend/ncclRecv for
-//            halos, ncclAllGather for the reduced system, ncclAllReduce for U.  NCCL is
+//            halos and for the two all-to-alls of the reduced system (scalars to the
+//            masters, y values back), ncclAllReduce for U.  NCCL is
 //            loaded at run time (the copy torch already loaded if present).
 #include <cuda_runtime.h>
 #include <dlfcn.h>
@@ -123,7 +124,16 @@ struct SlabArgs {
     const double* un[3];      // u^n (EPI_ADD_UN; SRC_DIV)
     const double* unew[3];    // u^{n+1} (SRC_DIV)
     double* p;                // SRC_DIV: p -> q = p - chi mu D.(u^{n+1}+u^n)/2
-    double* gather;           // [P][kSlots][plane]
+    // reduced-system exchange with a master rank per line (m = line mod P)
+    double* up_w;             // writer: this rank's block for master 0; + m * up_mstride for master m
+    long long up_mstride;
+    const double* up_r;       // master: [rank][Q][ns][nidx] it received (+ z * up_rmstride)
+    long long up_rmstride;
+    double* dn_w;             // master: block for rank 0; + r * dn_rstride for rank r (+ z * dn_wmstride)
+    long long dn_rstride, dn_wmstride;
+    const double* dn_r;       // rank: [master][comp][nb][nidx] it received
+    int nidx;                 // lines per master = plane / P
+    int nb;                   // values per rank, line and component returned: y_{rQ..rQ+Q}, corr
     double neg_rho_dt, chimu_half, invh;
     int n, nz, rank;
     int Q, Lseg;              // Schur parts per slab and their length (nz = Q Lseg)
@@ -195,12 +205,17 @@ __global__ void __launch_bounds__(128) k_slab_fwd(SlabCf C, SlabArgs A, int slot
         io[i * PL + q] = x;
         fsum += x;
     }
-    double* g = A.gather + ((long long)part * A.ns + slot0 + 2 * comp) * PL;
-    g[q] = d0 - b * x;                  // x = f*_1 here
-    g[PL + q] = fm;
-    if (MF) {
-        g[2 * PL + q] = dsum;
-        g[3 * PL + q] = fsum;
+    // to the line's master: [sub][slot][idx] in the block for master m
+    {
+        const int P = C.P / A.Q, mst = (int)(q % P);
+        const long long idx = q / P;
+        double* g = A.up_w + mst * A.up_mstride + ((long long)(part - A.rank * A.Q) * A.ns + slot0 + 2 * comp) * A.nidx + idx;
+        g[0] = d0 - b * x;              // x = f*_1 here
+        g[A.nidx] = fm;
+        if (MF) {
+            g[2 * (long long)A.nidx] = dsum;
+            g[3 * (long long)A.nidx] = fsum;
+        }
     }
 }
 
@@ -277,19 +292,22 @@ __global__ void __launch_bounds__(128) k_slab_fwd_reg(SlabCf C, SlabArgs A, int 
             io[i * PL + q] = d[i];
             fsum += d[i];
         }
-    double* g = A.gather + ((long long)part * A.ns + slot0 + 2 * comp) * PL;
-    g[q] = d[0] - b * d[1];
-    g[PL + q] = fm;
-    if (MF) {
-        g[2 * PL + q] = dsum;
-        g[3 * PL + q] = fsum;
+    {
+        const int P = C.P / A.Q, mst = (int)(q % P);
+        const long long idx = q / P;
+        double* g = A.up_w + mst * A.up_mstride + ((long long)(part - A.rank * A.Q) * A.ns + slot0 + 2 * comp) * A.nidx + idx;
+        g[0] = d[0] - b * d[1];
+        g[A.nidx] = fm;
+        if (MF) {
+            g[2 * (long long)A.nidx] = dsum;
+            g[3 * (long long)A.nidx] = fsum;
+        }
     }
 }
 
-// correction phase: r_t = A_t - c fm_{t-1} for every part t (all ranks' scalars are in
-// the gather buffer), y_s = (S^{-1} r)_s, y_{s+1}; x = f* - c y_s g - b y_{s+1} h; the
-// exact line-mean correction (R16) uses sum(y) = colsum(S^{-1}) . r and
-// sum(x) = (1 - c gsum - b hsum) sum(y) + sum_t F_t.
+// correction phase: with y_s, y_{s+1} and the line-mean correction returned by the line's
+// master (k_slab_master), x = f* - c y_s g - b y_{s+1} h (+ correction) on this part's
+// planes.
 template <int EPI, int MF>
 __global__ void __launch_bounds__(128) k_slab_corr(SlabCf C, SlabArgs A, int slot0)
 {
@@ -301,30 +319,16 @@ __global__ void __launch_bounds__(128) k_slab_corr(SlabCf C, SlabArgs A, int slo
     double* io = ((comp == 0) ? A.io[0] : (comp == 1 ? A.io[1] : A.io[2])) + k0 * A.plane;
     const double* un = ((comp == 0) ? A.un[0] : (comp == 1 ? A.un[1] : A.un[2])) + k0 * A.plane;
     const long long PL = A.plane;
-    const int P = C.P, s = part, s1 = (part + 1) % C.P;
-    slot0 += 2 * comp;                  // component c uses slots slot0 + 2c, slot0 + 2c + 1
+    const int P = C.P / A.Q;
     const double c = C.c(), b = C.b();
-    const double* SI = C.sinv();
-    const double* CS = C.colsum();
-    double ys = 0.0, ys1 = 0.0, ysum = 0.0, D = 0.0, F = 0.0;
-    for (int t = 0; t < P; ++t) {
-        const int tp = (t == 0) ? P - 1 : t - 1;
-        const double* gt = A.gather + ((long long)t * A.ns + slot0) * PL;
-        const double* gp = A.gather + ((long long)tp * A.ns + slot0) * PL;
-        const double r = gt[q] - c * gp[PL + q];
-        ys = fma(SI[s * P + t], r, ys);
-        ys1 = fma(SI[s1 * P + t], r, ys1);
-        if (MF) {
-            ysum = fma(CS[t], r, ysum);
-            D += gt[2 * PL + q];
-            F += gt[3 * PL + q];
-        }
-    }
-    double corr = 0.0;
-    if (MF) {
-        const double X = (1.0 - c * C.p[SC_GSUM] - b * C.p[SC_HSUM]) * ysum + F;
-        corr = (D * C.p[SC_INVROW] - X) / C.p[SC_N];
-    }
+    // y_s, y_{s+1} and the line-mean correction from the line's master
+    const int mst = (int)(q % P);
+    const long long idx = q / P;
+    const double* y = A.dn_r + ((long long)mst * 3 + comp) * A.nb * A.nidx + idx;
+    const int sub = part - A.rank * A.Q;
+    const double ys = y[(long long)sub * A.nidx], ys1 = y[(long long)(sub + 1) * A.nidx];
+    const double corr = MF ? y[(long long)(A.Q + 1) * A.nidx] : 0.0;
+    (void)slot0;
     const double* g = C.g();
     const double* h = C.h();
     const double cy = c * ys, by = b * ys1;
@@ -334,6 +338,57 @@ __global__ void __launch_bounds__(128) k_slab_corr(SlabCf C, SlabArgs A, int slo
         x += corr;
         if (EPI == EPI_ADD_UN) io[f] = un[f] + x;     // u^{n+1} = u^n + delta (R23)
         else io[f] = x;
+    }
+}
+
+// The reduced system of the lines a rank is master of (q = m + P idx): r_t = A_t -
+// c fm_{t-1} over the P Q parts t (every rank sent its scalars here), y_t = (S^{-1} r)_t,
+// the exact line-mean correction (R16: sum(y) = colsum(S^{-1}) . r and sum(x)
+// = (1 - c gsum - b hsum) sum(y) + sum_t F_t), and back to every rank r its
+// y_{rQ} .. y_{rQ+Q} and the correction.  A block takes 32 lines: r is staged in shared
+// memory once, the 8 warps split the rows t of S^{-1} (a row read is a warp broadcast).
+// blockIdx.z is the master among those this launch handles (all P with EMULATE, this
+// rank with NCCL).
+constexpr int kMasterWarps = 8;
+template <int MF>
+__global__ void __launch_bounds__(32 * kMasterWarps) k_slab_master(SlabCf C, SlabArgs A, int slot0)
+{
+    __shared__ double rs[kSlabMaxParts * 32];   // [t][lane]
+    const int lane = threadIdx.x & 31, tg = threadIdx.x >> 5;
+    const long long idx = blockIdx.x * 32LL + lane;
+    const bool ok = idx < A.nidx;
+    const int comp = blockIdx.y;
+    const int PQ = C.P, Q = A.Q, P = PQ / Q;
+    const double c = C.c(), b = C.b();
+    const double* SI = C.sinv();
+    const long long NI = A.nidx;
+    const double* in = A.up_r + (long long)blockIdx.z * A.up_rmstride;     // [rank][Q][ns][nidx]
+    auto slot = [&](int t, int k) -> double { return in[((long long)t * A.ns + slot0 + 2 * comp + k) * NI + idx]; };
+    for (int t = tg; t < PQ; t += kMasterWarps)
+        rs[t * 32 + lane] = ok ? slot(t, 0) - c * slot(t == 0 ? PQ - 1 : t - 1, 1) : 0.0;
+    __syncthreads();
+    if (!ok) return;
+    double* out = A.dn_w + (long long)blockIdx.z * A.dn_wmstride + (long long)comp * A.nb * NI + idx;
+    for (int t = tg; t < PQ; t += kMasterWarps) {
+        const double* row = SI + (long long)t * PQ;
+        double y = 0.0;
+        for (int u = 0; u < PQ; ++u) y = fma(row[u], rs[u * 32 + lane], y);
+        const int r = t / Q, j = t - r * Q;
+        out[(long long)r * A.dn_rstride + (long long)j * NI] = y;                 // y_{rQ+j} of rank r
+        if (j == 0)                                                               // y_{(r'+1)Q} of rank r' = r-1
+            out[(long long)((r + P - 1) % P) * A.dn_rstride + (long long)Q * NI] = y;
+    }
+    if (MF && tg == kMasterWarps - 1) {
+        const double* CS = C.colsum();
+        double ysum = 0.0, D = 0.0, F = 0.0;
+        for (int t = 0; t < PQ; ++t) {
+            ysum = fma(CS[t], rs[t * 32 + lane], ysum);
+            D += slot(t, 2);
+            F += slot(t, 3);
+        }
+        const double X = (1.0 - c * C.p[SC_GSUM] - b * C.p[SC_HSUM]) * ysum + F;
+        const double corr = (D * C.p[SC_INVROW] - X) / C.p[SC_N];
+        for (int r = 0; r < P; ++r) out[(long long)r * A.dn_rstride + (long long)(Q + 1) * NI] = corr;
     }
 }
 
@@ -361,27 +416,66 @@ static cudaError_t launch_fwd(Ctx* s, const SlabCf& C, const SlabArgs& a, int nc
     return cudaGetLastError();
 }
 
-static SlabArgs slab_args(Ctx* s, Group* G)
+// exchange layouts (ns slots per part, nb = Q + 2 values back per line and component):
+//   EMULATE  UP [master][rank][Q][ns][nidx], DN [rank][master][3][nb][nidx] (shared)
+//   NCCL     up_s [master][Q][ns][nidx] -> up_rv [rank][Q][ns][nidx] (all-to-all),
+//            dn_s [rank][3][nb][nidx]   -> dn_rv [master][3][nb][nidx]
+static SlabArgs slab_args(Ctx* s, Group* G, int ns)
 {
     SlabArgs a{};
-    a.gather = G->gather;
+    const int P = G->P, Q = G->Q;
     a.n = (int)s->n;
     a.nz = (int)s->nl;
     a.rank = s->rank;
-    a.Q = G->Q;
-    a.Lseg = (int)(s->nl / G->Q);
+    a.Q = Q;
+    a.Lseg = (int)(s->nl / Q);
     a.plane = s->plane;
     a.invh = 1.0 / s->h;
     a.neg_rho_dt = -s->rho / s->dt;
     a.chimu_half = 0.5 * s->chi * s->mu;
+    a.ns = ns;
+    a.nidx = (int)(s->plane / P);
+    a.nb = Q + 2;
+    const long long NI = a.nidx, blk = (long long)Q * ns * NI, blk2 = 3LL * a.nb * NI;
+    if (G->transport == IB_TRANSPORT_EMULATE) {
+        a.up_w = G->up_s + (long long)s->rank * blk;
+        a.up_mstride = (long long)P * blk;
+        a.up_r = G->up_s;
+        a.up_rmstride = (long long)P * blk;
+        a.dn_w = G->dn_s;
+        a.dn_wmstride = blk2;
+        a.dn_rstride = (long long)P * blk2;
+        a.dn_r = G->dn_s + (long long)s->rank * P * blk2;
+    } else {
+        a.up_w = G->up_s;
+        a.up_mstride = blk;
+        a.up_r = G->up_rv;
+        a.up_rmstride = 0;
+        a.dn_w = G->dn_s;
+        a.dn_wmstride = 0;
+        a.dn_rstride = blk2;
+        a.dn_r = G->dn_rv;
+    }
     return a;
+}
+
+// the masters' reduced systems of one solve (EMULATE: every master in one launch)
+cudaError_t slab_master(Ctx* s, Group* G, int sys, int ncomp, int ns, int mf)
+{
+    SlabArgs a = slab_args(s, G, ns);
+    SlabCf C{G->coef[sys], (int)(s->nl / G->Q) - 1, G->P * G->Q};
+    const unsigned nz = (G->transport == IB_TRANSPORT_EMULATE) ? (unsigned)G->P : 1u;
+    const dim3 grid((unsigned)((a.nidx + 31) / 32), (unsigned)ncomp, nz);
+    if (mf) k_slab_master<1><<<grid, 32 * kMasterWarps, 0, s->stream>>>(C, a, 0);
+    else k_slab_master<0><<<grid, 32 * kMasterWarps, 0, s->stream>>>(C, a, 0);
+    s->launches++;
+    return cudaGetLastError();
 }
 
 // viscous sweep along the cut axis, all components: st = u^n + (1 - A_last)^{-1} st
 cudaError_t slab_sweep_last_fwd(Ctx* s, Group* G)
 {
-    SlabArgs a = slab_args(s, G);
-    a.ns = 2 * s->dim;
+    SlabArgs a = slab_args(s, G, 2 * s->dim);
     for (int c = 0; c < s->dim; ++c) { a.io[c] = s->st[c]; a.un[c] = s->u[c]; }
     SlabCf C{G->coef[SYS_VISC], (int)(s->nl / G->Q) - 1, G->P * G->Q};
     if (s->dim == 3) return launch_fwd<3, SRC_FIELD, 0>(s, C, a, 3);
@@ -390,8 +484,7 @@ cudaError_t slab_sweep_last_fwd(Ctx* s, Group* G)
 
 cudaError_t slab_sweep_last_corr(Ctx* s, Group* G)
 {
-    SlabArgs a = slab_args(s, G);
-    a.ns = 2 * s->dim;
+    SlabArgs a = slab_args(s, G, 2 * s->dim);
     for (int c = 0; c < s->dim; ++c) { a.io[c] = s->st[c]; a.un[c] = s->u[c]; }
     SlabCf C{G->coef[SYS_VISC], (int)(s->nl / G->Q) - 1, G->P * G->Q};
     k_slab_corr<EPI_ADD_UN, 0><<<dim3(nb128(s->plane), (unsigned)s->dim, (unsigned)a.Q), 128, 0, s->stream>>>(C, a, 0);
@@ -402,8 +495,7 @@ cudaError_t slab_sweep_last_corr(Ctx* s, Group* G)
 // Step 3e RHS, explicit part of 3f and the psi factor along the cut axis (into p*)
 cudaError_t slab_divpsi_fwd(Ctx* s, Group* G)
 {
-    SlabArgs a = slab_args(s, G);
-    a.ns = 4;
+    SlabArgs a = slab_args(s, G, 4);
     a.io[0] = a.io[1] = a.io[2] = s->pstar;
     for (int c = 0; c < s->dim; ++c) { a.un[c] = s->u[c]; a.unew[c] = s->st[c]; }
     a.p = s->p;
@@ -414,8 +506,7 @@ cudaError_t slab_divpsi_fwd(Ctx* s, Group* G)
 
 cudaError_t slab_divpsi_corr(Ctx* s, Group* G)
 {
-    SlabArgs a = slab_args(s, G);
-    a.ns = 4;
+    SlabArgs a = slab_args(s, G, 4);
     a.io[0] = a.io[1] = a.io[2] = s->pstar;
     SlabCf C{G->coef[SYS_PSI], (int)(s->nl / G->Q) - 1, G->P * G->Q};
     k_slab_corr<EPI_STORE, 1><<<dim3(nb128(s->plane), 1, (unsigned)a.Q), 128, 0, s->stream>>>(C, a, 0);
@@ -426,8 +517,7 @@ cudaError_t slab_divpsi_corr(Ctx* s, Group* G)
 // stand-alone solve along the cut axis of data (in place) with coefficient block sys
 cudaError_t slab_user_fwd(Ctx* s, Group* G, double* data, int mf)
 {
-    SlabArgs a = slab_args(s, G);
-    a.ns = mf ? 4 : 2;
+    SlabArgs a = slab_args(s, G, mf ? 4 : 2);
     a.io[0] = a.io[1] = a.io[2] = data;
     SlabCf C{G->coef[SYS_USER], (int)(s->nl / G->Q) - 1, G->P * G->Q};
     if (mf) {
@@ -440,8 +530,7 @@ cudaError_t slab_user_fwd(Ctx* s, Group* G, double* data, int mf)
 
 cudaError_t slab_user_corr(Ctx* s, Group* G, double* data, int mf)
 {
-    SlabArgs a = slab_args(s, G);
-    a.ns = mf ? 4 : 2;
+    SlabArgs a = slab_args(s, G, mf ? 4 : 2);
     a.io[0] = a.io[1] = a.io[2] = data;
     SlabCf C{G->coef[SYS_USER], (int)(s->nl / G->Q) - 1, G->P * G->Q};
     const dim3 grid(nb128(s->plane), 1, (unsigned)a.Q);
@@ -763,12 +852,33 @@ int group_halo(Group* G, int nf, const HaloSpec* spec, cudaStream_t st)
     return 0;
 }
 
-// every rank's reduced-system scalars to every rank (EMULATE: the buffer is shared)
-int group_allgather(Group* G, int ns, cudaStream_t st)
+// each line's scalars to its master (all-to-all; EMULATE: the buffer is shared)
+int group_up(Group* G, int ns, cudaStream_t st)
 {
     if (G->transport == IB_TRANSPORT_EMULATE) return 0;
-    const size_t cnt = (size_t)G->Q * ns * G->slab[0]->plane;   // this rank's Q parts, ns slots each
-    return g_nccl.AllGather(G->gather + (size_t)G->rank * cnt, G->gather, cnt, kNcclDouble, G->comm, st);
+    const size_t blk = (size_t)G->Q * ns * (G->slab[0]->plane / G->P);
+    NCK(g_nccl.GroupStart());
+    for (int m = 0; m < G->P; ++m) {
+        NCK(g_nccl.Send(G->up_s + m * blk, blk, kNcclDouble, m, G->comm, st));
+        NCK(g_nccl.Recv(G->up_rv + m * blk, blk, kNcclDouble, m, G->comm, st));
+    }
+    NCK(g_nccl.GroupEnd());
+    return 0;
+}
+
+// the masters' y values and corrections back to the ranks (all-to-all)
+int group_dn(Group* G, int ncomp, cudaStream_t st)
+{
+    if (G->transport == IB_TRANSPORT_EMULATE) return 0;
+    const size_t NI = G->slab[0]->plane / G->P, nb = (size_t)G->Q + 2;
+    const size_t stride = 3 * nb * NI, cnt = (size_t)ncomp * nb * NI;
+    NCK(g_nccl.GroupStart());
+    for (int r = 0; r < G->P; ++r) {
+        NCK(g_nccl.Send(G->dn_s + r * stride, cnt, kNcclDouble, r, G->comm, st));
+        NCK(g_nccl.Recv(G->dn_rv + r * stride, cnt, kNcclDouble, r, G->comm, st));
+    }
+    NCK(g_nccl.GroupEnd());
+    return 0;
 }
 
 // U^n = sum over ranks of the partial interpolations
