@@ -626,19 +626,42 @@ bool pdl_enabled()
     return v == 1;
 }
 
-static int pick_r(const Ctx* s, int L, int nc)
+static int sm_count()
 {
-    static int forced = -1;
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n < 1) n = 148;
+    }
+    return n;
+}
+
+// lines per block R (a power of two): the largest whose tile fits (<= 100 KB for R >= 8,
+// i.e. >= 2 blocks per SM) and that still gives the grid >= minblk blocks: one per SM in
+// 2D, four per SM in 3D.  Measured (graph-mode ms/step): config 1 (256^2, 256 lines per
+// pass) 0.056 -> 0.025 (R 32/16 -> 1; one block per SM beats a few large tiles), config 2
+// 0.086 -> 0.076 (R 4), config 3 0.1974 -> 0.1959 (psi passes R 16), config 4 unchanged.
+static int pick_r(const Ctx* s, int L, int nc, int64_t rows, int64_t other)
+{
+    static int forced = -1, mb_env = -1;
     if (forced < 0) {
         const char* e = getenv("IBGM_R");
         forced = e ? atoi(e) : 0;
+        e = getenv("IBGM_MINBLK");
+        mb_env = e ? atoi(e) : 0;
     }
-    if (forced == 8 || forced == 16 || forced == 32) return forced;
-    for (int R = 32; R >= 8; R /= 2)
-        if (lines_smem(s->P, L, nc, R) <= 100 * 1024) return R;
-    for (int R = 4; R >= 1; R /= 2)     // long segments (2D N > 1024)
-        if (lines_smem(s->P, L, nc, R) <= 200 * 1024) return R;
-    return 1;
+    if (forced >= 1 && forced <= 32 && (forced & (forced - 1)) == 0 &&
+        lines_smem(s->P, L, nc, forced) <= (forced >= 8 ? 100 : 200) * 1024)
+        return forced;
+    const int64_t minblk = mb_env > 0 ? mb_env : (int64_t)sm_count() * (s->dim == 3 ? 4 : 1);
+    int best = 0;
+    for (int R = 32; R >= 1; R /= 2) {
+        if (lines_smem(s->P, L, nc, R) > (R >= 8 ? 100 : 200) * 1024) continue;
+        best = R;
+        if ((rows + R - 1) / R * other >= minblk) return R;
+    }
+    return best ? best : 1;
 }
 
 template <int L, int KIND, int DIM, int AX, int NC, int MINB>
@@ -661,7 +684,7 @@ template <int L, int KIND, int DIM, int AX, int NC, int MINB>
 static cudaError_t go_lines_k(Ctx* s, int sys, const LArgs& la, int ncomp_grid, int64_t rows, int gy)
 {
     auto kern = k_lines<L, KIND, DIM, AX, NC, MINB>;
-    const int R = pick_r(s, L, tiles_of(KIND, NC));
+    const int R = pick_r(s, L, tiles_of(KIND, NC), rows, (int64_t)gy * ncomp_grid);
     const size_t sm = lines_smem(s->P, L, tiles_of(KIND, NC), R);
     static unsigned long long attr_mask = 0;   // per instantiation, per device
     {
