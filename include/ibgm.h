@@ -198,13 +198,16 @@ int ib_get_stats(ib_ctx* ctx, int64_t* kernel_launches, int64_t* steps_done);
 
 /* Debug flags: bit 0 keeps the spread force f^{n+1/2} as a separate field so that
  * ib_get_aux can return it (costs one extra atomic per spread contribution and a
- * clear per step).  Bits 1-3 select the spreading method: 0 automatic (= 4),
+ * clear per step).  Bits 1-3 select the spreading method: 0 automatic (5 in 3D,
+ * 4 in 2D),
  * 1 one thread per point (4^d global fp64 reductions per component), 2 brick-binned
  * (points counting-sorted into 4^3-cell bricks every step, shared-memory tiles),
  * 3 box-staged (chunks of 64 consecutive points accumulate in a shared-memory box,
  * one global reduction per box node), 4 quad-lane (4 lanes per point and component,
- * one per x-node of a stencil row, so each warp reduction is coalesced).  Bits 4-5
- * select the interpolation: 0 automatic (= 1), 1 one thread per point, 2 box-staged,
+ * one per x-node of a stencil row, so each warp reduction is coalesced), 5 quad-lane
+ * with a warp pre-reduction (consecutive points of a warp with the same base node sum
+ * their contributions by shuffles and one lane group issues the reductions).  Bits 4-5
+ * select the interpolation: 0 automatic (3 in 2D, 1 in 3D), 1 one thread per point, 2 box-staged,
  * 3 quad-lane.  The points are kept internally in Morton order of their initial
  * cells (outputs are returned in the caller's order).  Automatic by default.  Only
  * the single-GPU path honours bits 1-5.  Set bit 0 before the first ib_step (or right

@@ -83,10 +83,11 @@ def test_line_solve_full_size_sampled_3d_384():
 # ------------------------------------------------------------------ one step, per stage
 @pytest.mark.parametrize("cfg,over", [(0, {}), (1, dict(n=64, pts=256)), (3, dict(n=32, nodes=2000)),
                                       (4, dict(n=48, nodes=1500)), (2, dict(n=128, pts=512))])
-@pytest.mark.parametrize("spread_mode,interp_mode", [(1, 1), (2, 2), (3, 3), (4, 0)])
+@pytest.mark.parametrize("spread_mode,interp_mode", [(1, 1), (2, 2), (3, 3), (4, 0), (5, 3)])
 def test_one_step_stage_parity(cfg, over, spread_mode, interp_mode):
     """After one step: X^{n+1/2}, F^{n+1/2}, spread f, N(u^n), then u, p, psi, X -- with
-    every spreading method (per-point, brick-binned, box-staged, quad-lane) and every
+    every spreading method (per-point, brick-binned, box-staged, quad-lane, quad-lane with
+    warp pre-reduction) and every
     interpolation path (per-point, box-staged, quad-lane)."""
     from paper_1305_3976_b200 import inputs
     pr = inputs.config(cfg, **over)
@@ -114,6 +115,7 @@ def test_one_step_stage_parity(cfg, over, spread_mode, interp_mode):
 # ------------------------------------------------------------------ 10 steps, configs
 @pytest.mark.parametrize("cfg,over,mode", [(0, {}, 0), (1, {}, 0), (2, {}, 0), (3, {}, 0), (3, {}, 2), (3, {}, 1),
                                            (4, dict(n=96, nodes=4000), 0), (4, dict(n=96, nodes=4000), 2),
+                                           (4, dict(n=96, nodes=4000), 5),
                                            (2, dict(n=128, pts=256, kernel=1), 0)])
 def test_ten_step_parity(cfg, over, mode):
     """End-to-end bar of the north_star: rel L_inf <= 1e-9 on u, p and X after 10 steps.
