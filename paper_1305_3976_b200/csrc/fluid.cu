@@ -601,6 +601,125 @@ __global__ void __launch_bounds__(256, MINB) k_lines(const LineCoef C, const Sch
     LP::store(tile, tile2, A, n, R, TP, g0, tb, comp, threadIdx.x, blockDim.x);
 }
 
+// -------------------------------------------------------------------------------
+// Strided-line pass (y / z lines, and y in 2D): one thread per (line, part).  A block
+// holds RI neighbouring lines (consecutive i) x P parts; warp w covers RI lines of one
+// part, so each of a thread's L loads is one coalesced RI-wide row.  The part stays in
+// registers: Thomas on its interior, the interface values and the
+// reduced right-hand side go through a small shared array (4 barriers), y = S^{-1} r,
+// correction and the exact line-mean correction (R16) -- the
+// arithmetic of ws_solve with shared memory in place of the lane shuffles, and no
+// staged tile.
+// -------------------------------------------------------------------------------
+template <int L, int KIND, int DIM, int AX>
+__global__ void __launch_bounds__(512) k_strided(const LineCoef C, const SchurInv* __restrict__ SI, int n, int RI,
+                                                 LArgs A)
+{
+    static_assert(AX != 0, "x lines use the tiled pass");
+    constexpr int M = L - 1;
+    extern __shared__ double smem[];
+    const int P = C.P;
+    double* sinvT = smem;
+    double* xl = sinvT + P * P;          // [P][RI] last interior value f*_{s,m}
+    double* rr = xl + P * RI;            // [P][RI] reduced right-hand side r_s
+    double* yb = rr + P * RI;            // [P][RI] y_s
+    double* ds = yb + P * RI;            // [P][RI] line sums of d (mean correction)
+    double* xs = ds + P * RI;            // [P][RI] line sums of x
+    load_sinvT(sinvT, SI, P);
+    const int il = threadIdx.x % RI, s = threadIdx.x / RI;
+    const int i = blockIdx.x * RI + il;
+    const int comp = (KIND == K_DIVPSI) ? 0 : blockIdx.z;
+    const unsigned N = (unsigned)n;
+    const unsigned S = (AX == 1) ? N : N * N;                     // stride along the line
+    const unsigned base = (unsigned)i + ((AX == 1) ? ((DIM == 3) ? N * N * blockIdx.y : 0u) : N * blockIdx.y);
+    const unsigned q0 = base + S * (unsigned)(s * L);
+    double x[L];
+    double un[L];
+    if (KIND == K_DIVPSI) {
+        // D.u^{n+1} and D.u^n at the part's cells; Step 3e RHS and the
+        // explicit part of Step 3f
+        const unsigned stp[3] = {1u, N, N * N};
+#pragma unroll
+        for (int j = 0; j < L; ++j) {
+            const unsigned q = q0 + S * (unsigned)j;
+            int ijk[3];
+            ijk[0] = i;
+            if (AX == 1) { ijk[1] = s * L + j; ijk[2] = 0; } else { ijk[1] = (int)blockIdx.y; ijk[2] = s * L + j; }
+            double dn = 0.0, dol = 0.0;
+#pragma unroll
+            for (int c = 0; c < DIM; ++c) {
+                const unsigned qp = (ijk[c] == n - 1) ? q - (N - 1) * stp[c] : q + stp[c];
+                const double* unw = pick3<const double*>(A.unew[0], A.unew[1], A.unew[2], c);
+                const double* uo = pick3<const double*>(A.un[0], A.un[1], A.un[2], c);
+                dn += ldg(unw + qp) - ldg(unw + q);
+                dol += ldg(uo + qp) - ldg(uo + q);
+            }
+            dn *= A.invh;
+            dol *= A.invh;
+            x[j] = A.neg_rho_dt * dn;
+            A.p[q] = A.p[q] - A.chimu_half * (dn + dol);
+        }
+    } else {
+        const double* src = pick3<double*>(A.io[0], A.io[1], A.io[2], comp);
+#pragma unroll
+        for (int j = 0; j < L; ++j) x[j] = ldg(src + q0 + S * (unsigned)j);
+        if (KIND == K_LAST) {
+            const double* u0 = pick3<const double*>(A.un[0], A.un[1], A.un[2], comp);
+#pragma unroll
+            for (int j = 0; j < L; ++j) un[j] = ldg(u0 + q0 + S * (unsigned)j);
+        }
+    }
+    const double c = C.c, b = C.b;
+    const bool mf = C.mean_fix != 0;
+    double dsum = 0.0;
+    if (mf) {
+#pragma unroll
+        for (int j = 0; j < L; ++j) dsum += x[j];
+    }
+    x[1] *= C.inv[0];
+#pragma unroll
+    for (int j = 2; j <= M; ++j) x[j] = (x[j] - c * x[j - 1]) * C.inv[j - 1];
+#pragma unroll
+    for (int j = M - 1; j >= 1; --j) x[j] -= C.cp[j - 1] * x[j + 1];
+    const int sp = (s == 0) ? P - 1 : s - 1, sn = (s == P - 1) ? 0 : s + 1;
+    xl[s * RI + il] = x[M];
+    if (mf) ds[s * RI + il] = dsum;
+    __syncthreads();
+    rr[s * RI + il] = x[0] - c * xl[sp * RI + il] - b * x[1];
+    __syncthreads();
+    double ys = 0.0;
+    for (int q = 0; q < P; ++q) ys = fma(sinvT[q * P + s], rr[q * RI + il], ys);
+    yb[s * RI + il] = ys;
+    __syncthreads();
+    const double ys1 = yb[sn * RI + il];
+    x[0] = ys;
+    const double cy = c * ys, by = b * ys1;
+#pragma unroll
+    for (int j = 1; j <= M; ++j) x[j] -= cy * C.g[j - 1] + by * C.h[j - 1];
+    if (mf) {
+        double t = 0.0;
+#pragma unroll
+        for (int j = 0; j < L; ++j) t += x[j];
+        xs[s * RI + il] = t;
+        __syncthreads();
+        double D = 0.0, X = 0.0;
+        for (int q = 0; q < P; ++q) {
+            D += ds[q * RI + il];
+            X += xs[q * RI + il];
+        }
+        const double corr = (D * C.inv_rowsum - X) * C.inv_n;
+#pragma unroll
+        for (int j = 0; j < L; ++j) x[j] += corr;
+    }
+    double* dst = (KIND == K_DIVPSI) ? A.io[0] : pick3<double*>(A.io[0], A.io[1], A.io[2], comp);
+#pragma unroll
+    for (int j = 0; j < L; ++j) {
+        const unsigned q = q0 + S * (unsigned)j;
+        if (KIND == K_LAST) dst[q] = un[j] + x[j];            // u^{n+1} = u^n + delta (R23)
+        else dst[q] = x[j];
+    }
+}
+
 __global__ void k_sub(const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ o, size_t cnt)
 {
     for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < cnt; q += (size_t)gridDim.x * blockDim.x)
@@ -642,6 +761,17 @@ static int sm_count()
 // 2D, four per SM in 3D.  Measured (graph-mode ms/step): config 1 (256^2, 256 lines per
 // pass) 0.056 -> 0.025 (R 32/16 -> 1; one block per SM beats a few large tiles), config 2
 // 0.086 -> 0.076 (R 4), config 3 0.1974 -> 0.1959 (psi passes R 16), config 4 unchanged.
+// y / z passes by k_strided (IBGM_STRIDED=0: the tiled k_lines pass, for A/B)
+static bool strided_enabled()
+{
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("IBGM_STRIDED");
+        v = (e && atoi(e) == 0) ? 0 : 1;
+    }
+    return v == 1;
+}
+
 static int pick_r(const Ctx* s, int L, int nc, int64_t rows, int64_t other)
 {
     static int forced = -1, mb_env = -1;
@@ -675,6 +805,20 @@ static cudaError_t go_lines(Ctx* s, int sys, const LArgs& a, int ncomp_grid)
     LArgs la = a;
     la.nl = (int)s->nl;
     la.wrap = s->wrap;
+    if constexpr (AX != 0 && L <= 16 && (KIND == K_MID || KIND == K_LAST || KIND == K_DIVPSI)) {
+        if (strided_enabled()) {
+            const int RI = (s->P <= 16) ? 32 : 16;
+            if (s->n % RI == 0 && s->P * RI <= 512) {
+                auto kern = k_strided<L, KIND, DIM, AX>;
+                const size_t sm = ((size_t)s->P * s->P + 5 * (size_t)s->P * RI) * sizeof(double);
+                const int gy = (DIM == 3) ? (int)s->nl : 1;
+                const dim3 grid((unsigned)(s->n / RI), (unsigned)gy, (unsigned)ncomp_grid);
+                kern<<<grid, s->P * RI, sm, s->stream>>>(s->hcoef[sys], s->sinv + sys, (int)s->n, RI, la);
+                s->launches++;
+                return cudaGetLastError();
+            }
+        }
+    }
     const int64_t rows = (AX == 0 && DIM == 2) ? s->nl : s->n;
     const int gy = (DIM == 3) ? (int)s->nl : 1;
     return go_lines_k<L, KIND, DIM, AX, NC, (KIND == K_S1 || L >= 24) ? 2 : 4>(s, sys, la, ncomp_grid, rows, gy);
