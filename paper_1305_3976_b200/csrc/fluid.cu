@@ -29,6 +29,7 @@
 // drained with coalesced global accesses (consecutive x for every axis).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 
@@ -805,9 +806,18 @@ static cudaError_t go_lines(Ctx* s, int sys, const LArgs& a, int ncomp_grid)
     LArgs la = a;
     la.nl = (int)s->nl;
     la.wrap = s->wrap;
-    if constexpr (AX != 0 && L <= 16 && (KIND == K_MID || KIND == K_LAST || KIND == K_DIVPSI)) {
+    // (the divergence pass stays tiled: strided it measured 35.3 -> 41.4 us at config 3,
+    //  995 -> 1335 us at config 4 -- twelve gathers per cell, all before the solve)
+    if constexpr (AX != 0 && L <= 16 && (KIND == K_MID || KIND == K_LAST)) {
         if (strided_enabled()) {
-            const int RI = (s->P <= 16) ? 32 : 16;
+            static int ri_env = -1;
+            if (ri_env < 0) {
+                const char* e = getenv("IBGM_RI");
+                ri_env = e ? atoi(e) : 0;
+            }
+            // 256 threads per block: RI = 256 / P lines (measured: config 3 RI 16 0.1777 vs
+            // 32 0.1818 ms/step; config 4 z sweep RI 8 771 vs 16 882 us)
+            const int RI = ri_env > 0 ? ri_env : std::max(8, std::min(32, 256 / s->P));
             if (s->n % RI == 0 && s->P * RI <= 512) {
                 auto kern = k_strided<L, KIND, DIM, AX>;
                 const size_t sm = ((size_t)s->P * s->P + 5 * (size_t)s->P * RI) * sizeof(double);
