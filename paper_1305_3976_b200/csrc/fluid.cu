@@ -374,6 +374,7 @@ struct LArgs {
     double neg_rho_dt, chimu_half, invh;
     int nl;                 // local planes of the last axis (N, or the slab depth)
     int wrap;               // 1: the last axis is periodic here; 0: z-slab with halo planes
+    int s1flat;             // S1 fill flattened over the tile's cells when n >= threads
 };
 
 // Visit every (line l, position m) of a tile with coalesced global offsets: consecutive
@@ -418,7 +419,26 @@ struct LinePass {
         const unsigned RTP = (unsigned)R * TP;
         const int nrow = (DIM == 2) ? A.nl : n;
         if (KIND == K_S1) {
-            if (n >= T) {
+            if (n >= T && A.s1flat) {
+                // the tile's R x n cells flattened over the threads (n = 384 on 256 threads:
+                // 12 cells each instead of two rounds per row with half the threads idle)
+                const int lmax = min(R, nrow - g0);
+                const int tot = lmax * n;
+                for (int e = t; e < tot; e += T) {
+                    const int l = e / n, m = e - l * n;
+                    const int ep = e + IBGM_PF_DIST * T;
+                    if (ep < tot) {
+                        const int lp = ep / n;
+                        s1_prefetch<DIM>(A.s1, ep - lp * n, row_bases<DIM>(g0 + lp, (int)tb, n, A.nl, A.wrap));
+                    }
+                    const RowB rb = row_bases<DIM>(g0 + l, (int)tb, n, A.nl, A.wrap);
+                    double v[3];
+                    s1_cell<DIM>(A.s1, m, rb, n, v);
+                    const int off = tile_off<L>(l, m, TP);
+#pragma unroll
+                    for (int c = 0; c < NC; ++c) tile[c * RTP + off] = v[c];
+                }
+            } else if (n >= T) {
                     for (int l = 0; l < R && g0 + l < nrow; ++l) {
                     const RowB rb = row_bases<DIM>(g0 + l, (int)tb, n, A.nl, A.wrap);
                     if (l + IBGM_PF_ROWS < R && g0 + l + IBGM_PF_ROWS < nrow) {
@@ -806,6 +826,14 @@ static cudaError_t go_lines(Ctx* s, int sys, const LArgs& a, int ncomp_grid)
     LArgs la = a;
     la.nl = (int)s->nl;
     la.wrap = s->wrap;
+    {
+        static int fl = -1;
+        if (fl < 0) {
+            const char* e = getenv("IBGM_S1FLAT");
+            fl = (e && atoi(e) == 0) ? 0 : 1;
+        }
+        la.s1flat = fl;
+    }
     // (the divergence pass stays tiled: strided it measured 35.3 -> 41.4 us at config 3,
     //  995 -> 1335 us at config 4 -- twelve gathers per cell, all before the solve)
     if constexpr (AX != 0 && L <= 16 && (KIND == K_MID || KIND == K_LAST)) {
