@@ -26,7 +26,8 @@ def phase_of(name, grid):
         return "force"
     if name.startswith("k_spread") or name.startswith("k_brick"):
         return "spread"
-    if name.startswith("k_lines"):
+    if name.startswith("k_lines") or name.startswith("k_strided"):
+        # k_lines<L, KIND, DIM, AX, ...>, k_strided<L, KIND, DIM, AX>
         args = [a.strip() for a in name[name.index("<") + 1:name.index(">")].split(",")]
         kind, ax = int(args[1]), int(args[3])
         if kind == 0:
