@@ -206,13 +206,14 @@ int ib_get_stats(ib_ctx* ctx, int64_t* kernel_launches, int64_t* steps_done);
  * one global reduction per box node), 4 quad-lane (4 lanes per point and component,
  * one per x-node of a stencil row, so each warp reduction is coalesced), 5 quad-lane
  * with a warp pre-reduction (consecutive points of a warp with the same base node sum
- * their contributions by shuffles and one lane group issues the reductions).  Bits 4-5
- * select the interpolation: 0 automatic (3 in 2D, 1 in 3D), 1 one thread per point, 2 box-staged,
- * 3 quad-lane.  The points are kept internally in Morton order of their initial
+ * their contributions by shuffles and one lane group issues the reductions).  Bits 4-6
+ * select the interpolation: 0 automatic (3 in 2D, 4 in 3D), 1 one thread per point, 2 box-staged,
+ * 3 quad-lane, 4 one thread per (point, component).  The points are kept internally in Morton order of their initial
  * cells (outputs are returned in the caller's order).  Automatic by default.  Only
- * the single-GPU path honours bits 1-5.  Set bit 0 before the first ib_step (or right
+ * the single-GPU path honours bits 1-6.  Set bit 0 before the first ib_step (or right
  * after ib_set_fields): once the look-ahead has run the next step's IB phase, turning
- * it on returns IB_ESTATE. */
+ * it on returns IB_ESTATE.  Errors: IB_EINVAL (spreading method > 5, interpolation
+ * method > 4, or a bit above 6 set). */
 int ib_set_debug(ib_ctx* ctx, int32_t flags);
 
 /* Turn per-phase CUDA-event timing on (1) or off (0).  While on, ib_step records an

@@ -999,6 +999,9 @@ int ib_set_debug(ib_ctx* c, int32_t flags)
 {
     if (!c) return fail(IB_EINVAL, "null context");
     Ctx* s = &c->s;
+    if (((flags >> 1) & 7) > 5 || ((flags >> 4) & 7) > 4 || (flags >> 7) != 0)
+        return fail(IB_EINVAL, "debug flags 0x%x: spreading method > 5, interpolation method > 4 or unknown bits",
+                    (unsigned)flags);
     const int keep = (flags & 1) != 0;
     if (keep && !s->debug_keep_f && s->ib_ahead)
         return fail(IB_ESTATE, "set debug bit 0 before stepping: the next step's IB phase has already run");
@@ -1010,7 +1013,7 @@ int ib_set_debug(ib_ctx* c, int32_t flags)
     drop_graphs(s);
     s->debug_keep_f = keep;
     s->spread_mode = (flags >> 1) & 7;   // bits 1-3: spreading method (include/ibgm.h)
-    s->interp_mode = (flags >> 4) & 3;   // bits 4-5: interpolation method
+    s->interp_mode = (flags >> 4) & 7;   // bits 4-6: interpolation method
     return IB_OK;
 }
 

@@ -99,6 +99,69 @@ __global__ void k_interp_evolve(const double* __restrict__ u0, const double* __r
     }
 }
 
+// The same Steps 1a-1c with one thread per (point, component): a 64 * DIM block holds
+// 64 points, warp group c interpolates component c of all of them (3x the threads of
+// k_interp_evolve at a third of the registers); the block barrier orders every read of
+// X^n before the writes of X^{n+1}.
+template <int DIM, int KER>
+__global__ void __launch_bounds__(64 * DIM) k_interp_comp(const double* __restrict__ u0, const double* __restrict__ u1,
+                                                        const double* __restrict__ u2, double* __restrict__ X,
+                                                        double* __restrict__ Xh, double* __restrict__ Uprev,
+                                                        double* __restrict__ Xold, double* __restrict__ Uold,
+                                                        int64_t npts, int n, double invh, double dt, int first)
+{
+    const int c = threadIdx.x >> 6;
+    const int64_t k = blockIdx.x * 64LL + (threadIdx.x & 63);
+    const bool ok = k < npts;
+    double Xk[3] = {0, 0, 0};
+    if (ok) {
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) Xk[a] = X[k * DIM + a];
+    }
+    __syncthreads();
+    if (!ok) return;
+    const double* uc = (c == 0) ? u0 : (c == 1 ? u1 : u2);
+    const size_t nn = (size_t)n;
+    int i0[3] = {0, 0, 0};
+    double w[3][4];
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) weights4<KER>(Xk[a] * invh - (a == c ? 0.0 : 0.5), n, i0[a], w[a]);
+    double acc = 0.0;
+    if (DIM == 2) {
+#pragma unroll
+        for (int m1 = 0; m1 < 4; ++m1) {
+            const size_t row = nn * (size_t)wrap1(i0[1] + m1, n);
+            double r = 0.0;
+#pragma unroll
+            for (int m0 = 0; m0 < 4; ++m0) r += w[0][m0] * uc[row + wrap1(i0[0] + m0, n)];
+            acc += w[1][m1] * r;
+        }
+    } else {
+#pragma unroll
+        for (int m2 = 0; m2 < 4; ++m2) {
+            const size_t pl = nn * nn * (size_t)wrap1(i0[2] + m2, n);
+            double pa = 0.0;
+#pragma unroll
+            for (int m1 = 0; m1 < 4; ++m1) {
+                const size_t row = pl + nn * (size_t)wrap1(i0[1] + m1, n);
+                double r = 0.0;
+#pragma unroll
+                for (int m0 = 0; m0 < 4; ++m0) r += w[0][m0] * uc[row + wrap1(i0[0] + m0, n)];
+                pa += w[1][m1] * r;
+            }
+            acc += w[2][m2] * pa;
+        }
+    }
+    const double xc = (c == 0) ? Xk[0] : (c == 1 ? Xk[1] : Xk[2]);
+    const double up = Uprev[k * DIM + c];
+    const double xn = first ? xc + dt * acc : xc + dt * (1.5 * acc - 0.5 * up);
+    Xh[k * DIM + c] = 0.5 * (xn + xc);
+    X[k * DIM + c] = xn;
+    Uprev[k * DIM + c] = acc;
+    Xold[k * DIM + c] = xc;
+    Uold[k * DIM + c] = up;
+}
+
 // Step 2a: F_k = sum_{e=(k,m)} kappa_e (X_m - X_k)(1 - L_e/|X_m - X_k|) at X^{n+1/2}
 // (PAPER.md:607-614 in the force-connection form of PAPER.md:856-861), gathered per
 // point from a CSR adjacency (no atomics).  X_m - X_k is the minimum-image displacement
@@ -970,9 +1033,10 @@ static cudaError_t box_attr(K kern, size_t sm)
 cudaError_t launch_interp_evolve(Ctx* s, int first)
 {
     if (s->npts == 0) return cudaSuccess;
-    // auto: quad-lane in 2D (config 2 0.0762 -> 0.0748 ms/step), per point in 3D (quad
-    // 0.1954 -> 0.2009 on config 3)
-    const int im = s->interp_mode ? s->interp_mode : (s->dim == 2 ? 3 : 1);
+    // auto: quad-lane in 2D (config 2 0.0762 -> 0.0748 ms/step), per (point, component)
+    // in 3D (config 3 interp 20.4 -> 19.5 us, config 4 172 -> 162 us; quad-lane there:
+    // 0.1954 -> 0.2009 ms/step)
+    const int im = s->interp_mode ? s->interp_mode : (s->dim == 2 ? 3 : 4);
     if (im == 3) {
         const int64_t thr = ((s->npts + 7) / 8) * 8 * s->dim * 4;
         const unsigned nbk = (unsigned)((thr + 255) / 256);
@@ -1003,8 +1067,18 @@ cudaError_t launch_interp_evolve(Ctx* s, int first)
         s->launches++;
         return cudaGetLastError();
     }
-    const int thr = 128;
     const double invh = 1.0 / s->h;
+    if (im == 4) {
+        const unsigned nb = (unsigned)((s->npts + 63) / 64);
+#define IBGM_IC(D, K) k_interp_comp<D, K><<<nb, 64 * D, 0, s->stream>>>(s->u[0], s->u[1], s->u[2], s->X, s->Xh, \
+        s->Uprev, s->Xold, s->Uold, s->npts, (int)s->n, invh, s->dt, first)
+        if (s->dim == 2) { if (s->kernel == IB_DELTA_COS4) IBGM_IC(2, 0); else IBGM_IC(2, 1); }
+        else { if (s->kernel == IB_DELTA_COS4) IBGM_IC(3, 0); else IBGM_IC(3, 1); }
+#undef IBGM_IC
+        s->launches++;
+        return cudaGetLastError();
+    }
+    const int thr = 128;
 #define IBGM_IE(D, K) launch_pdl_if(D == 2, k_interp_evolve<D, K>, dim3(nblk(s->npts, thr)), dim3(thr), 0, s->stream, \
         s->u[0], s->u[1], s->u[2], s->X, s->Xh, s->Uprev, s->Xold, s->Uold, s->npts, (int)s->n, invh, s->dt, first)
     if (s->dim == 2) { if (s->kernel == IB_DELTA_COS4) IBGM_IE(2, 0); else IBGM_IE(2, 1); }

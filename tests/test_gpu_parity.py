@@ -83,12 +83,12 @@ def test_line_solve_full_size_sampled_3d_384():
 # ------------------------------------------------------------------ one step, per stage
 @pytest.mark.parametrize("cfg,over", [(0, {}), (1, dict(n=64, pts=256)), (3, dict(n=32, nodes=2000)),
                                       (4, dict(n=48, nodes=1500)), (2, dict(n=128, pts=512))])
-@pytest.mark.parametrize("spread_mode,interp_mode", [(1, 1), (2, 2), (3, 3), (4, 0), (5, 3)])
+@pytest.mark.parametrize("spread_mode,interp_mode", [(1, 1), (2, 2), (3, 3), (4, 0), (5, 3), (5, 4)])
 def test_one_step_stage_parity(cfg, over, spread_mode, interp_mode):
     """After one step: X^{n+1/2}, F^{n+1/2}, spread f, N(u^n), then u, p, psi, X -- with
     every spreading method (per-point, brick-binned, box-staged, quad-lane, quad-lane with
     warp pre-reduction) and every
-    interpolation path (per-point, box-staged, quad-lane)."""
+    interpolation path (per-point, box-staged, quad-lane, per (point, component))."""
     from paper_1305_3976_b200 import inputs
     pr = inputs.config(cfg, **over)
     o = _oracle_for(pr)
