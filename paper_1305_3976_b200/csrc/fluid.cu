@@ -684,7 +684,7 @@ __global__ void __launch_bounds__(512) k_strided(const LineCoef C, const SchurIn
         const double* src = pick3<double*>(A.io[0], A.io[1], A.io[2], comp);
 #pragma unroll
         for (int j = 0; j < L; ++j) x[j] = ldg(src + q0 + S * (unsigned)j);
-        if (KIND == K_LAST) {
+        if (KIND == K_LAST && L <= 16) {    // (longer parts load u^n in the epilogue)
             const double* u0 = pick3<const double*>(A.un[0], A.un[1], A.un[2], comp);
 #pragma unroll
             for (int j = 0; j < L; ++j) un[j] = ldg(u0 + q0 + S * (unsigned)j);
@@ -736,7 +736,8 @@ __global__ void __launch_bounds__(512) k_strided(const LineCoef C, const SchurIn
 #pragma unroll
     for (int j = 0; j < L; ++j) {
         const unsigned q = q0 + S * (unsigned)j;
-        if (KIND == K_LAST) dst[q] = un[j] + x[j];            // u^{n+1} = u^n + delta (R23)
+        if (KIND == K_LAST)                                     // u^{n+1} = u^n + delta (R23)
+            dst[q] = (L <= 16 ? un[j] : ldg(pick3<const double*>(A.un[0], A.un[1], A.un[2], comp) + q)) + x[j];
         else dst[q] = x[j];
     }
 }
@@ -836,7 +837,7 @@ static cudaError_t go_lines(Ctx* s, int sys, const LArgs& a, int ncomp_grid)
     }
     // (the divergence pass stays tiled: strided it measured 35.3 -> 41.4 us at config 3,
     //  995 -> 1335 us at config 4 -- twelve gathers per cell, all before the solve)
-    if constexpr (AX != 0 && L <= 16 && (KIND == K_MID || KIND == K_LAST)) {
+    if constexpr (AX != 0 && L <= 32 && (KIND == K_MID || KIND == K_LAST)) {
         if (strided_enabled()) {
             static int ri_env = -1;
             if (ri_env < 0) {
@@ -844,8 +845,9 @@ static cudaError_t go_lines(Ctx* s, int sys, const LArgs& a, int ncomp_grid)
                 ri_env = e ? atoi(e) : 0;
             }
             // 256 threads per block: RI = 256 / P lines (measured: config 3 RI 16 0.1777 vs
-            // 32 0.1818 ms/step; config 4 z sweep RI 8 771 vs 16 882 us)
-            const int RI = ri_env > 0 ? ri_env : std::max(8, std::min(32, 256 / s->P));
+            // 32 0.1818 ms/step; config 4 z sweep RI 8 771 vs 16 882 us); 512 for L = 32
+            // (config 2 y sweep: RI 16 13.0 us, 8 14.8, 4 20.4; tiled 25.0)
+            const int RI = ri_env > 0 ? ri_env : std::max(8, std::min(32, (L > 16 ? 512 : 256) / s->P));
             if (s->n % RI == 0 && s->P * RI <= 512) {
                 auto kern = k_strided<L, KIND, DIM, AX>;
                 const size_t sm = ((size_t)s->P * s->P + 5 * (size_t)s->P * RI) * sizeof(double);

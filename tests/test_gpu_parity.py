@@ -245,6 +245,21 @@ def test_step_before_set_fields_is_an_error():
     ctx.close()
 
 
+def test_debug_flags_out_of_range_are_rejected():
+    """ib_set_debug: spreading method > 5, interpolation method > 4 or unknown bits are
+    IB_EINVAL (include/ibgm.h), and leave the context usable."""
+    from paper_1305_3976_b200 import ibgm
+    ctx = ibgm.Context(2, 32, 0.01, 1.0, 1e-3)
+    for spread, interp in ((6, 0), (7, 0), (0, 5), (0, 7)):
+        with pytest.raises(ibgm.IBGMError) as e:
+            ctx.set_debug(False, spread, interp)
+        assert e.value.code == -1
+    ctx.set_debug(False, 5, 4)
+    ctx.set_fields(np.zeros((32, 32)), np.zeros((32, 32)))
+    ctx.step(1)
+    ctx.close()
+
+
 def test_nonfinite_is_detected():
     from paper_1305_3976_b200 import ibgm
     n = 16
