@@ -794,7 +794,7 @@ static bool strided_enabled()
     return v == 1;
 }
 
-static int pick_r(const Ctx* s, int L, int nc, int64_t rows, int64_t other)
+static int pick_r(const Ctx* s, int L, int nc, int64_t rows, int64_t other, int per_sm = 0)
 {
     static int forced = -1, mb_env = -1;
     if (forced < 0) {
@@ -806,7 +806,7 @@ static int pick_r(const Ctx* s, int L, int nc, int64_t rows, int64_t other)
     if (forced >= 1 && forced <= 32 && (forced & (forced - 1)) == 0 &&
         lines_smem(s->P, L, nc, forced) <= (forced >= 8 ? 100 : 200) * 1024)
         return forced;
-    const int64_t minblk = mb_env > 0 ? mb_env : (int64_t)sm_count() * (s->dim == 3 ? 4 : 1);
+    const int64_t minblk = mb_env > 0 ? mb_env : (int64_t)sm_count() * (per_sm > 0 ? per_sm : (s->dim == 3 ? 4 : 1));
     int best = 0;
     for (int R = 32; R >= 1; R /= 2) {
         if (lines_smem(s->P, L, nc, R) > (R >= 8 ? 100 : 200) * 1024) continue;
@@ -868,7 +868,20 @@ template <int L, int KIND, int DIM, int AX, int NC, int MINB>
 static cudaError_t go_lines_k(Ctx* s, int sys, const LArgs& la, int ncomp_grid, int64_t rows, int gy)
 {
     auto kern = k_lines<L, KIND, DIM, AX, NC, MINB>;
-    const int R = pick_r(s, L, tiles_of(KIND, NC), rows, (int64_t)gy * ncomp_grid);
+    // the divergence + first psi factor pass: two blocks per SM suffice in 3D (config 3:
+    // R 32 31.4 us vs R 16 35.3 us, 0.1716 -> 0.1680 ms/step; config 4 keeps R 16 -- its
+    // R 32 tile exceeds the 100 KB two-blocks-per-SM bound and measured 1261 vs 998 us)
+    int R = pick_r(s, L, tiles_of(KIND, NC), rows, (int64_t)gy * ncomp_grid, (KIND == K_DIVPSI && DIM == 3) ? 2 : 0);
+    {
+        static int rk = -2;
+        if (rk == -2) {
+            char nm[32];
+            snprintf(nm, sizeof(nm), "IBGM_R_K%d", KIND);
+            const char* e = getenv(nm);
+            rk = e ? atoi(e) : 0;
+        }
+        if (rk > 0 && lines_smem(s->P, L, tiles_of(KIND, NC), rk) <= 200 * 1024) R = rk;
+    }
     const size_t sm = lines_smem(s->P, L, tiles_of(KIND, NC), R);
     static unsigned long long attr_mask = 0;   // per instantiation, per device
     {
