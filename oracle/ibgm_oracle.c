@@ -23,6 +23,9 @@
  *             identity + 2nd-order convergence), cyclic solves (dense LU),
  *             viscous Douglas sweeps (Stokes Taylor-Green closed form),
  *             psi / p pipeline (per-Fourier-mode linear recurrence), start-up,
+ *             time integration (Step 1c midpoint in uniform flow, Step 1b AB2 order
+ *             from tracer self-convergence, eq. (nonlinear) AB2 advection from the
+ *             explicit increment u* - u^n via the orc_keep_ustar test hook),
  *             minimum-image force connections (R26: through-the-boundary spring
  *             equals its nearby image), box side H (R2: the 2x2 ellipse array on
  *             [0,2]^2 equals the tiled single ellipse), and the whole method against
@@ -419,6 +422,8 @@ typedef struct {
     int64_t* edges;
     double *kappa, *rest;
     long step;
+    int keep_ustar;              /* test hook: keep u* and p* of the last step */
+    double *ustar[3], *pstar;
 } orc_state;
 
 void orc_destroy(orc_state* s);
@@ -462,7 +467,8 @@ orc_state* orc_create_box(int dim, long n, double H, double mu, double rho, doub
 void orc_destroy(orc_state* s)
 {
     if (!s) return;
-    for (int c = 0; c < 3; c++) { free(s->u[c]); free(s->nprev[c]); free(s->nadv[c]); free(s->f[c]); free(s->ws[c]); }
+    for (int c = 0; c < 3; c++) { free(s->u[c]); free(s->nprev[c]); free(s->nadv[c]); free(s->f[c]); free(s->ws[c]); free(s->ustar[c]); }
+    free(s->pstar);
     free(s->p); free(s->psi); free(s->r);
     free(s->X); free(s->Xh); free(s->Xn); free(s->U); free(s->Uprev); free(s->F); free(s->wgt);
     free(s->edges); free(s->kappa); free(s->rest);
@@ -558,7 +564,9 @@ static void one_step(orc_state* s)
             double nhalf = (n == 0) ? s->nadv[c][q] : 1.5 * s->nadv[c][q] - 0.5 * s->nprev[c][q];
             s->ws[c][q] = s->u[c][q] + dt * (-nhalf + (mu * lap - op_grad(g, s->r, i, j, k, c) + s->f[c][q]) / rho);
         }
+        if (s->keep_ustar) memcpy(s->ustar[c], s->ws[c], sizeof(double) * nc);
     }
+    if (s->keep_ustar) memcpy(s->pstar, s->r, sizeof(double) * nc);
 
     /* Steps 3c, 3d (and z in 3D): Douglas direction-split Crank-Nicolson sweeps
      *   (1 - (mu dt / 2 rho) D_aa) u^{(a)} = u^{(a-1)} - (mu dt / 2 rho) D_aa u^n
@@ -644,3 +652,29 @@ void orc_get_aux(const orc_state* s, double* fu, double* fv, double* fw, double*
 }
 
 long orc_steps_done(const orc_state* s) { return s->step; }
+
+/* Test hook: from now on keep u* (the explicit momentum result of Step 3b, before
+ * the Douglas sweeps) and p* (Step 3a) of each step.  Returns -1 on allocation
+ * failure.  Storage only -- no arithmetic changes. */
+int orc_keep_ustar(orc_state* s)
+{
+    if (s->keep_ustar) return 0;
+    for (int c = 0; c < s->g.dim; c++) {
+        s->ustar[c] = (double*)calloc(s->nc, sizeof(double));
+        if (!s->ustar[c]) return -1;
+    }
+    s->pstar = (double*)calloc(s->nc, sizeof(double));
+    if (!s->pstar) return -1;
+    s->keep_ustar = 1;
+    return 0;
+}
+
+/* u* (per component) and p* of the last step; requires orc_keep_ustar() first. */
+int orc_get_ustar(const orc_state* s, double* us, double* vs, double* ws, double* pstar)
+{
+    if (!s->keep_ustar) return -1;
+    double* o[3] = {us, vs, ws};
+    for (int c = 0; c < s->g.dim; c++) if (o[c]) memcpy(o[c], s->ustar[c], sizeof(double) * s->nc);
+    if (pstar) memcpy(pstar, s->pstar, sizeof(double) * s->nc);
+    return 0;
+}

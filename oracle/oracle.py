@@ -38,7 +38,9 @@ _lib = None
 def lib():
     global _lib
     if _lib is None:
-        _lib = ctypes.CDLL(build())
+        # IBGM_ORACLE_LIB: load a prebuilt variant (tools/oracle_mutants.py builds
+        # deliberately broken copies to show each pin fails on them)
+        _lib = ctypes.CDLL(os.environ.get("IBGM_ORACLE_LIB") or build())
         L = _lib
         L.orc_phi.restype = ctypes.c_double
         L.orc_phi.argtypes = [ctypes.c_int, ctypes.c_double]
@@ -72,6 +74,10 @@ def lib():
         L.orc_step.argtypes = [ctypes.c_void_p, ctypes.c_long]
         L.orc_get_fields.argtypes = [ctypes.c_void_p, _dp, _dp, _dp, _dp, _dp, _dp, _dp]
         L.orc_get_aux.argtypes = [ctypes.c_void_p, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp]
+        L.orc_keep_ustar.restype = ctypes.c_int
+        L.orc_keep_ustar.argtypes = [ctypes.c_void_p]
+        L.orc_get_ustar.restype = ctypes.c_int
+        L.orc_get_ustar.argtypes = [ctypes.c_void_p, _dp, _dp, _dp, _dp]
         L.orc_steps_done.restype = ctypes.c_long
         L.orc_steps_done.argtypes = [ctypes.c_void_p]
     return _lib
@@ -228,6 +234,20 @@ class Oracle:
         lib().orc_get_fields(self._h, _p(u[0]), _p(u[1]), _p(u[2]) if self.dim == 3 else None,
                              _p(p), _p(psi), _p(X) if self.npts else None, _p(U) if self.npts else None)
         return dict(u=u, p=p, psi=psi, X=X, U=U)
+
+    def keep_ustar(self):
+        """Test hook: keep u* (Step 3b) and p* (Step 3a) of every following step."""
+        if lib().orc_keep_ustar(self._h) != 0:
+            raise MemoryError("orc_keep_ustar failed")
+
+    def ustar(self):
+        shp = _shape(self.dim, self.n)
+        us = [np.empty(shp) for _ in range(self.dim)]
+        ps = np.empty(shp)
+        rc = lib().orc_get_ustar(self._h, _p(us[0]), _p(us[1]), _p(us[2]) if self.dim == 3 else None, _p(ps))
+        if rc != 0:
+            raise RuntimeError("call keep_ustar() before stepping")
+        return dict(ustar=us, pstar=ps)
 
     def aux(self):
         shp = _shape(self.dim, self.n)
