@@ -1,18 +1,22 @@
 #!/usr/bin/env python
 """bench.py -- fluid+IB grid-point updates per second (fp64) of the IB-GM step on B200.
 
-Default workload: BASELINE.json configs[3] (3D, 128^3 MAC grid, one triangulated
-ellipsoidal shell of ~40k nodes, rho=1, mu=0.01, dt=1e-4) -- the largest
-configuration that is defined for a single GPU (configs[4] is the 8-GPU z-slab
-case); see DESIGN.md "Measurement".  One "step" = one full IB-GM time step
+Workload at every N: BASELINE.json configs[4] (3D, 384^3 MAC grid, eight triangulated
+ellipsoidal shells of 100k nodes each, random divergence-free initial velocity,
+rho=1, mu=0.005, dt=5e-5) -- the configuration BASELINE names for the 8-GPU z-slab
+split; it also fits one B200 (~6 GB of fields), so the driver's per-N values form
+one strong-scaling curve.  configs[2] (2D, 1024^2) and configs[3] (3D, 128^3) are
+reported under "extra" with the same keys.  One "step" = one full IB-GM time step
 (Steps 1a-3f) on the whole grid.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C]
 
-Prints ONE JSON line on rank 0.  value = N^d * steps / (max over ranks of the device
-time of the K timed steps).  With N GPUs (torchrun) the same grid is cut into N
-z-slabs, one per rank, over NCCL (strong scaling).  Inputs (17 resident fp64 fields, ~285 MB at 128^3)
-are larger than the 126 MB L2, so no explicit L2 flush is done between steps.
+`--gpus N` (N > 1) outside torchrun relaunches itself under torch.distributed.run with
+N ranks on 127.0.0.1.  Prints ONE JSON line on rank 0.  value = N^d * steps / (max
+over ranks of the device time of the K timed steps).  With N GPUs the same grid is
+cut into N z-slabs, one per rank, over NCCL (strong scaling).  The
+resident fields (14 fp64 fields: 235 MB at 128^3, 6.3 GB at 384^3) are larger than
+the 126 MB L2, so no explicit L2 flush is done between steps.
 """
 from __future__ import annotations
 
@@ -42,12 +46,14 @@ ALG_DOUBLES = {
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the configs[2]/[3] extra lines")
+    ap.add_argument("--dry-run", action="store_true", help="launch plumbing only: print each rank's view, exit")
     return ap.parse_args()
 
 
@@ -160,22 +166,27 @@ def max_over_ranks(x: float) -> float:
     return float(t.item())
 
 
-def cpu_baseline(cfg, steps=2):
-    """The oracle as it stands, single-threaded, on a bounded sample: `steps` full
-    time steps of the same workload (after one untimed step)."""
+def cpu_baseline(cfg):
+    """The oracle as it stands, single-threaded, on a bounded sample of the same
+    workload: whole time steps (the oracle's unit of work), one untimed step first when
+    a step is short; a config-4 step (~1 min) is timed alone."""
     from oracle import oracle as O
     from paper_1305_3976_b200 import inputs
     pr = inputs.config(cfg)
     o = O.Oracle(pr.dim, pr.n, pr.mu, pr.rho, pr.dt, chi=pr.chi, kernel=pr.kernel)
     o.set_fields(*pr.u, p=pr.p) if pr.dim == 3 else o.set_fields(pr.u[0], pr.u[1], None, pr.p)
     o.set_boundary(pr.X, pr.edges, pr.kappa, rest=pr.rest, weight=pr.weight)
-    o.step(1)
+    big = pr.ncell > 4_000_000
+    steps = 1 if big else 2
+    if not big:
+        o.step(1)
     t0 = time.perf_counter()
     o.step(steps)
     dt = time.perf_counter() - t0
     return {"value": pr.ncell * steps / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{steps} full oracle time steps of config {cfg} ({pr.n}^{pr.dim} cells, "
-                      f"{pr.npts} IB points) after 1 untimed step; single-threaded C (oracle/ibgm_oracle.c)",
+            "sample": f"{steps} full oracle time step(s) of configs[{cfg}] ({pr.n}^{pr.dim} cells, "
+                      f"{pr.npts} IB points){'' if big else ' after 1 untimed step'}; single-threaded C "
+                      f"(oracle/ibgm_oracle.c)",
             "seconds": dt}
 
 
@@ -191,16 +202,21 @@ def run_reference(args):
     o.set_fields(*pr.u, p=pr.p) if pr.dim == 3 else o.set_fields(pr.u[0], pr.u[1], None, pr.p)
     o.set_boundary(pr.X, pr.edges, pr.kappa, rest=pr.rest, weight=pr.weight)
     t0 = time.perf_counter()
-    o.step(1)                       # one warm-up step (the oracle has no warm-up effects)
+    o.step(1)                       # first step (the oracle has no warm-up effects)
     t1 = time.perf_counter() - t0
     budget = 150.0                  # keep the whole run within a few minutes
-    k = max(1, min(args.steps, int(budget / max(t1, 1e-3))))
-    t0 = time.perf_counter()
-    o.step(k)
-    dt = time.perf_counter() - t0
+    if t1 > 20.0:
+        # a long step (config 4: ~1 min) is itself the bounded sample
+        k, dt, warm = 1, t1, 0
+    else:
+        k = max(1, min(args.steps, int(budget / max(t1, 1e-3))))
+        t0 = time.perf_counter()
+        o.step(k)
+        dt = time.perf_counter() - t0
+        warm = 1
     v = pr.ncell * k / dt
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-           "steps": k, "warmup": 1, "ms_per_step": 1e3 * dt / k, "higher_is_better": True,
+           "steps": k, "warmup": warm, "ms_per_step": 1e3 * dt / k, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": arm_config(pr, args.config, world),
            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
@@ -209,41 +225,42 @@ def run_reference(args):
     print(json.dumps(out), flush=True)
 
 
-def main():
-    args = parse()
-    if args.impl == "reference":
-        return run_reference(args)
-    import numpy as np
-    import torch
-    rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl")
-    from paper_1305_3976_b200 import ibgm, inputs
-    pr = inputs.config(args.config)
-    dim, n = pr.dim, pr.n
-    # a dedicated (non-default) stream: the library enqueues every kernel on it and the
-    # timing events below are recorded on the same stream
-    stream = torch.cuda.Stream()
-    torch.cuda.set_stream(stream)
-    assert stream.cuda_stream != 0
+def relaunch_under_torchrun(args):
+    """`bench.py --gpus N` (N > 1) outside torchrun: start N ranks on this node with
+    torch.distributed.run (127.0.0.1 rendezvous) and return their exit code."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    print("bench.py: relaunching under torchrun:", " ".join(cmd), file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
+def measure(ibgm, inputs, torch, cfg, steps, warmup, rank, world, local, stream, keep_ctx=False, clock=None):
+    """Time `steps` graph-replayed steps of configs[cfg] (device time on the library's
+    stream, max over ranks), then the same steps with per-phase event pairs for the
+    roofline attribution.  Returns (record, ctx or None, problem)."""
+    pr = inputs.config(cfg)
     if world > 1:
         # z-slab decomposition over the ranks (SURVEY.md §8(e)): NCCL transport, the
         # unique id broadcast over the process group
         nccl_id = ibgm.share_nccl_id()
         ctx = ibgm.from_problem(pr, device=local, stream=stream.cuda_stream, nranks=world, rank=rank,
                                 nccl_id=nccl_id)
+        print(f"bench.py: rank {rank}/{world} NCCL communicator up (configs[{cfg}], slab of {pr.n // world} planes)",
+              file=sys.stderr, flush=True)
     else:
         ctx = ibgm.from_problem(pr, device=local, stream=stream.cuda_stream)
+    dim = pr.dim
     ncl = pr.ncell // world          # cells this rank holds
 
     def barrier():
         if world > 1:
             torch.distributed.barrier()
 
-    # warm-up
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         ctx.step(1)
     ctx.sync()
     torch.cuda.synchronize()
@@ -253,22 +270,26 @@ def main():
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        e0.record(stream)
-        for _ in range(args.steps):
-            ctx.step(1)
-        e1.record(stream)
-        torch.cuda.synchronize()
+    clk = ClockSampler(local) if clock else None
+    if clk:
+        clk.__enter__()
+    e0.record(stream)
+    for _ in range(steps):
+        ctx.step(1)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if clk:
+        clk.__exit__()
     barrier()
+    ctx.sync()                       # also surfaces any device-raised fault
     ms = max_over_ranks(e0.elapsed_time(e1))
     launches = ctx.stats()["kernel_launches"] - l0
     # every step updates the whole N^d grid (each rank its slab): strong scaling
-    updates = float(pr.ncell) * args.steps
-    value = updates / (ms * 1e-3)
+    value = float(pr.ncell) * steps / (ms * 1e-3)
 
-    # --- timed region B: the same K steps with per-phase event pairs (roofline attribution)
+    # --- timed region B: the same steps with per-phase event pairs (roofline attribution)
     ctx.set_profiling(True)
-    kb = max(10, min(args.steps, 200))
+    kb = max(10, min(steps, 200))
     ctx.step(kb)
     ctx.sync()
     ph = ctx.phase_times()
@@ -280,62 +301,119 @@ def main():
     peak, peak_src = measured_peaks()
     achieved = alg / (dom_ms * 1e-3) / 1e9
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", f"traffic_cfg{args.config}.json")
+    tpath = os.path.join(ROOT, "profiles", f"traffic_cfg{cfg}.json")
     if os.path.exists(tpath):
         traffic = json.load(open(tpath)).get(dom)
     step_alg = sum(ALG_DOUBLES[dim][k] for k in ALG_DOUBLES[dim] if k in ph) * 8 * ncl
     phases = {k: {"ms": round(v[0] / v[1], 5), "share": round(v[0] / tot_ph, 4),
                   "alg_gbs": (round(ALG_DOUBLES[dim][k] * 8 * ncl / (v[0] / v[1] * 1e-3) / 1e9, 1)
-                              if k in ALG_DOUBLES[dim] else None)} for k, v in ph.items()}
+                              if k in ALG_DOUBLES[dim] else None),
+                  "frac": (round(ALG_DOUBLES[dim][k] * 8 * ncl / (v[0] / v[1] * 1e-3) / 1e9 / peak, 3)
+                           if k in ALG_DOUBLES[dim] else None)} for k, v in ph.items()}
+    rec = {"value": value, "unit": UNIT, "ms_per_step": ms / steps, "steps": steps, "warmup": warmup,
+           "config": arm_config(pr, cfg, world),
+           "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                        "frac": achieved / peak, "traffic": traffic,
+                        "alg_bytes_per_launch": alg, "peak_source": peak_src,
+                        "step_frac": step_alg / (ms / steps * 1e-3) / 1e9 / peak},
+           "phases": phases, "gpu_launches": launches}
+    if clk:
+        rec["clocks"] = clk.summary()
+    if keep_ctx:
+        return rec, ctx, pr
+    ctx.close()
+    return rec, None, pr
 
-    # --- e2e through the public API with pinned host buffers
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args))
+    if args.dry_run:
+        # launch plumbing only (CPU test of the relaunch): report what this rank sees
+        print(json.dumps({"dry_run": True, "impl": args.impl, "rank": rank, "world_size": world,
+                          "local_rank": local, "gpus": args.gpus}), flush=True)
+        return
+    if args.impl == "reference":
+        return run_reference(args)
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    import torch
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    from paper_1305_3976_b200 import ibgm, inputs
+    # a dedicated (non-default) stream: the library enqueues every kernel on it and the
+    # timing events are recorded on the same stream
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    assert stream.cuda_stream != 0
+
+    head, ctx, pr = measure(ibgm, inputs, torch, args.config, args.steps, args.warmup, rank, world, local, stream,
+                            keep_ctx=True, clock=True)
+    dim = pr.dim
+
+    # --- e2e through the public API with pinned host buffers: every step uploads the
+    # complete solver state (ib_set_state: u, the momentum history, p, p*, X, U -- what
+    # the next step reads), advances one step and downloads the new state (ib_get_state),
+    # so each e2e step is exactly a regular step of the time integration
     e2e = None
     if not args.no_e2e:
-        pin = lambda shape: torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()  # noqa: E731
-        hu = [pin(ctx.shape) for _ in range(dim)]
-        hp = pin(ctx.shape)
-        hX = pin((pr.npts, dim))
-        ctx.get_fields_into(hu[0], hu[1], hu[2] if dim == 3 else None, hp, hX)
-        ke = max(3, min(args.steps, 20))
+        nb = ctx.state_size()
+        blob = torch.empty(nb, dtype=torch.uint8, pin_memory=True).numpy()
+        ctx.get_state(blob)
+        ke = max(3, min(args.steps, 10))
+        ctx.set_state(blob)
+        ctx.step(1)
+        ctx.get_state(blob)              # untimed warm-up of the copy path
         torch.cuda.synchronize()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(stream)
         for _ in range(ke):
-            ctx.set_fields(hu[0], hu[1], hu[2] if dim == 3 else None, hp)   # H2D of the step's inputs
+            ctx.set_state(blob)          # H2D of the step's inputs (the state)
             ctx.step(1)
-            ctx.get_fields_into(hu[0], hu[1], hu[2] if dim == 3 else None, hp, hX)  # D2H of the result
+            ctx.get_state(blob)          # D2H of the step's result (the new state)
         f1.record(stream)
         torch.cuda.synchronize()
         ems = max_over_ranks(f0.elapsed_time(f1))
         e2e = {"value": float(pr.ncell) * ke / (ems * 1e-3), "unit": UNIT,
-               "h2d_bytes_per_step": (dim + 1) * pr.ncell * 8,
-               "d2h_bytes_per_step": (dim + 1) * pr.ncell * 8 + world * pr.npts * dim * 8,
-               "steps": ke, "note": "per step: ib_set_fields (H2D u,v,[w],p from pinned) + ib_step(1) + "
-                                    "ib_get_fields (D2H u,v,[w],p,X to pinned)"}
+               "h2d_bytes_per_step": nb, "d2h_bytes_per_step": nb, "steps": ke,
+               "note": "per step: ib_set_state (H2D of the full solver state from pinned memory) + ib_step(1) + "
+                       "ib_get_state (D2H of the new state to pinned memory); bytes per rank"}
+    ctx.close()
+
+    # --- the other 2D/3D configurations as extra lines (north_star: 2D and 3D numbers)
+    extra = {}
+    if not args.no_extra:
+        for c in (2, 3):
+            if c == args.config:
+                continue
+            rec, _, _ = measure(ibgm, inputs, torch, c, max(20, min(args.steps, 200)), max(3, args.warmup), rank,
+                                world, local, stream)
+            extra[f"configs[{c}]"] = rec
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args.config, steps=2 if pr.ncell <= 4_000_000 else 1)
+        cpu = cpu_baseline(args.config)
 
     if rank == 0:
         out = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "metric": METRIC, "value": head["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": arm_config(pr, args.config, world),
-            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "alg_bytes_per_launch": alg, "peak_source": peak_src,
-                         "step_frac": step_alg / (ms / args.steps * 1e-3) / 1e9 / peak},
-            "phases": phases,
-            "gpu_launches": launches,
+            "config": head["config"],
+            "roofline": head["roofline"],
+            "phases": head["phases"],
+            "gpu_launches": head["gpu_launches"],
             "e2e": e2e,
             "cpu_baseline": cpu,
-            "clocks": clk.summary(),
+            "clocks": head["clocks"],
+            "extra": extra,
         }
         print(json.dumps(out), flush=True)
-    ctx.close()
     if world > 1:
         torch.distributed.destroy_process_group()
 

@@ -48,12 +48,16 @@ extern "C" {
 
 #define IB_OK 0
 #define IB_EINVAL (-1)      /* invalid argument (dim, N, dt, rho, nu, chi, edge index ...) */
-#define IB_ESTATE (-2)      /* ib_step before ib_set_fields                                  */
+#define IB_ESTATE (-2)      /* call out of order (ib_step before ib_set_fields, ...)           */
 #define IB_ECUDA (-3)       /* a CUDA runtime call failed (message names it)                  */
 #define IB_ENCCL (-4)       /* NCCL could not be loaded or an NCCL call failed                */
-#define IB_ENONFINITE (-5)  /* NaN/Inf detected in the state by ib_check_finite               */
-#define IB_EDOMAIN (-6)     /* reserved: IB point left the rank's slab + halo                 */
+#define IB_ENONFINITE (-5)  /* NaN/Inf in u, p or X (ib_check_finite, or the in-step check)    */
+#define IB_EDOMAIN (-6)     /* an IB point moved more than one cell h in one step, so its
+                               4-point support left the halo a step assumes (
+                               an explicit-coupling stability failure: reduce dt)            */
 #define IB_ENOMEM (-7)      /* device allocation failed                                       */
+#define IB_EDEGENERATE (-8) /* a force connection with rest length L != 0 has zero length
+                               |X_m - X_k| = 0: singular strain                 */
 
 #define IB_TRANSPORT_NCCL 0     /* one slab per process, one process per GPU (nranks > 1) */
 #define IB_TRANSPORT_EMULATE 1  /* all nranks slabs in this context, one GPU               */
@@ -108,7 +112,10 @@ int ib_create(const ib_grid* grid, double nu, double rho, double dt, const ib_op
 
 /* Set the initial state: velocity u^0, v^0, (w^0: NULL in 2D) on the MAC faces and
  * pressure p^{-1/2} (NULL -> 0); psi^{-1/2} = 0 and the step counter is reset to 0,
- * which arms the start-up rules of PAPER.md:686-697.  Each array is N^d doubles. */
+ * which arms the start-up rules of PAPER.md:686-697.  Each array is N^d doubles.
+ * The immersed boundary keeps its current position X^n (the one ib_get_fields
+ * returns); a look-ahead IB phase already run for the next step is undone.  Clears
+ * raised faults. */
 int ib_set_fields(ib_ctx* ctx, const double* u, const double* v, const double* w,
                   const double* p);
 
@@ -131,11 +138,43 @@ int ib_set_fibers(ib_ctx* ctx, int32_t n_fibers, const int64_t* pts_per_fiber,
 
 /* Advance nsteps time steps (Steps 1a-3f each).  All work is enqueued on the
  * context's stream; the call returns after enqueueing (use ib_sync to wait).
- * Errors: IB_ESTATE (no ib_set_fields yet), IB_ECUDA. */
+ * Device-detected faults are sticky: the force kernel raises IB_EDEGENERATE (a
+ * connection with L != 0 and zero length; its force is dropped instead of spreading
+ * NaN), and every K-th step (ib_set_check_interval, default K = 100) a state check
+ * raises IB_ENONFINITE (NaN/Inf in u, p or X) or IB_EDOMAIN (a point moved more than
+ * h).  A raised fault is returned by the first ib_step / ib_sync / ib_get_state after
+ * the kernel that raised it has run (ib_step checks on entry and after enqueueing,
+ * without waiting), and by every later ib_step until ib_set_fields, ib_set_state or
+ * ib_set_boundary clears it.  With the NCCL transport each rank detects its own
+ * faults; a rank that reports one must abort the job (the others would wait in the
+ * next collective).  Errors: IB_ESTATE (no ib_set_fields yet), IB_ECUDA, IB_ENCCL,
+ * IB_EDEGENERATE, IB_ENONFINITE, IB_EDOMAIN. */
 int ib_step(ib_ctx* ctx, int64_t nsteps);
 
-/* Block until all work enqueued on the context's stream has completed. */
+/* Run the in-step state check (see ib_step) every `every` steps; 0 turns it off.
+ * Default 100.  The check reads u, p and X once (~4 fields of traffic).
+ * Errors: IB_EINVAL (every < 0). */
+int ib_set_check_interval(ib_ctx* ctx, int64_t every);
+
+/* Block until all work enqueued on the context's stream has completed; then return
+ * any device-raised fault (see ib_step). */
 int ib_sync(ib_ctx* ctx);
+
+/* Checkpoint / resume: the complete state the next step reads (u^n, the momentum
+ * history G = N(u^{n-1}) [+ (2/rho) f^{n+3/2} once the look-ahead ran], p^{n-1/2},
+ * p* = p^{n-1/2} + psi^{n-1/2}, X^n, U^{n-1}, the look-ahead's X^{n+1}/U^n, the step
+ * counter) as an opaque host blob of ib_state_size bytes, valid for a context with the
+ * same grid, parameters, decomposition and rank and the same immersed boundary
+ * (ib_set_boundary with the same points).  ib_set_state followed by ib_step(k) gives
+ * bit for bit the steps the saving context would have taken (same kernels, same
+ * order; spreading atomics aside, R18).  Both synchronise the stream
+ * before returning (the buffer may be reused at once).  ib_set_state clears any
+ * raised fault.  Errors: IB_EINVAL (null, buffer too small, blob of another
+ * grid/parameters/decomposition/boundary), IB_ESTATE (ib_get_state before
+ * ib_set_fields), IB_ECUDA. */
+int ib_state_size(ib_ctx* ctx, int64_t* bytes);
+int ib_get_state(ib_ctx* ctx, void* buf, int64_t bytes);
+int ib_set_state(ib_ctx* ctx, const void* buf, int64_t bytes);
 
 /* Copy the state to host buffers (any pointer may be NULL): u^n, v^n, w^n,
  * p^{n-1/2}, psi^{n-1/2} (N^d each), X^n and U^{n-1} (the velocity interpolated in
@@ -176,12 +215,15 @@ int ib_line_solve(ib_ctx* ctx, int32_t axis, double kappa, const double* d, doub
  * Errors: IB_EINVAL (repeats < 1, null f/psi, slab context). */
 int ib_psi_solve(ib_ctx* ctx, const double* f, double* psi, int32_t repeats, double* device_ms);
 
-/* Device-side finiteness check of u, p and X; IB_ENONFINITE if any NaN/Inf. */
+/* Synchronous device-side finiteness check of u, p and X now; IB_ENONFINITE if any
+ * NaN/Inf (independent of the sticky in-step faults). */
 int ib_check_finite(ib_ctx* ctx);
 
-/* Number of kernels this library launched since the context was created, and the
- * number of completed steps. */
-int ib_get_stats(ib_ctx* ctx, int64_t* kernel_launches, int64_t* steps_done);
+/* Statistics (any pointer may be NULL): ms_per_phase[IB_NPHASES] the average device
+ * milliseconds per step of each phase over the steps timed since ib_set_profiling(1)
+ * (0 for phases never timed; see the IB_PH_* list), the number of completed steps, and
+ * the number of kernels this library launched since the context was created. */
+int ib_get_stats(ib_ctx* ctx, double* ms_per_phase, int64_t* steps_done, int64_t* kernel_launches);
 
 /* Phases of one step, for ib_get_phase_times (one kernel launch each). */
 #define IB_PH_INTERP 0   /* Steps 1a-1c: interpolate U^n, evolve X                         */

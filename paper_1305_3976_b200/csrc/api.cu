@@ -329,6 +329,63 @@ static cudaError_t points_out(Ctx* s, const double* dev, double* host)
                            s->stream);
 }
 
+// default interval of the in-step state check (ib_set_check_interval)
+static const int64_t kDefaultCheckEvery = 100;
+
+// the sticky errors raised by kernels (k_force: degenerate connection; the periodic
+// state check: non-finite values, a point moving more than a cell).  The words are
+// mapped host memory written with plain device stores, so a flag becomes visible once
+// the kernel that raised it has run; IB_OK if none is set.
+static int poll_errors(Ctx* s)
+{
+    volatile int* e = s->err_h;
+    if (!e) return IB_OK;
+    if (e[ERR_DEGENERATE])
+        return fail(IB_EDEGENERATE, "a force connection with rest length L != 0 has zero length |X_m - X_k| = 0 "
+                                    "(singular strain, SPEC.md:140); the state is suspect from step <= %lld on",
+                    (long long)s->step);
+    if (e[ERR_NONFINITE]) return fail(IB_ENONFINITE, "non-finite value in u, p or X (in-step check, <= %lld steps)",
+                                      (long long)s->step);
+    if (e[ERR_DOMAIN])
+        return fail(IB_EDOMAIN, "an immersed-boundary point moved more than one cell h in one step (<= %lld steps): "
+                                "the 4-point support left its halo (SPEC.md:131); reduce dt", (long long)s->step);
+    return IB_OK;
+}
+
+static void clear_errors(Ctx* s)
+{
+    if (s->err_h) memset((void*)s->err_h, 0, ERR_WORDS * sizeof(int));
+}
+
+// the in-step state check: every field held by the context (or its slabs) and X for
+// non-finite values, X^{n+1} - X^{n+1/2} for a move of more than a cell
+static cudaError_t enqueue_check(Ctx* s)
+{
+    const int ns = s->grp ? s->grp->nloc : 0;
+    for (int r = 0; r < ns; ++r) {
+        cudaError_t e = launch_check_finite(s->grp->slab[r], s->err_d + ERR_NONFINITE);
+        if (e != cudaSuccess) return e;
+    }
+    cudaError_t e = launch_check_finite(s, s->err_d + ERR_NONFINITE);
+    if (e == cudaSuccess) e = launch_check_domain(s, s->err_d + ERR_DOMAIN);
+    return e;
+}
+
+// With the look-ahead the device already holds X^{n+1}, U^n (and the IB history of
+// step n+1); Xold/Uold keep X^n, U^{n-1}.  Put the state of step n back before
+// anything restarts the time stepping from it.
+static cudaError_t undo_lookahead(Ctx* s)
+{
+    if (s->ib_ahead && s->npts > 0) {
+        const size_t pb = (size_t)s->npts * s->dim * sizeof(double);
+        cudaError_t e = cudaMemcpyAsync(s->X, s->Xold, pb, cudaMemcpyDeviceToDevice, s->stream);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(s->Uprev, s->Uold, pb, cudaMemcpyDeviceToDevice, s->stream);
+        if (e != cudaSuccess) return e;
+    }
+    s->ib_ahead = false;
+    return cudaSuccess;
+}
+
 extern "C" {
 
 void ib_default_options(ib_options* o)
@@ -426,6 +483,10 @@ int ib_create(const ib_grid* grid, double nu, double rho, double dt, const ib_op
     *out = c;
 
     CKC(cudaSetDevice(o.device));
+    CKC(cudaHostAlloc((void**)&s->err_h, ERR_WORDS * sizeof(int), cudaHostAllocMapped));
+    memset(s->err_h, 0, ERR_WORDS * sizeof(int));
+    CKC(cudaHostGetDevicePointer((void**)&s->err_d, s->err_h, 0));
+    s->check_every = kDefaultCheckEvery;
     if (o.stream) {
         s->stream = (cudaStream_t)o.stream;
         s->own_stream = false;
@@ -490,6 +551,8 @@ int ib_create(const ib_grid* grid, double nu, double rho, double dt, const ib_op
             sl->stream = s->stream; sl->own_stream = false;
             sl->L = L; sl->P = Pseg;
             sl->sinv = s->sinv;
+            sl->err_h = s->err_h;
+            sl->err_d = s->err_d;
             memcpy(sl->hcoef, s->hcoef, sizeof(s->hcoef));
             sl->rank = (o.transport == IB_TRANSPORT_EMULATE) ? r : o.rank;
             sl->nl = nz;
@@ -581,9 +644,11 @@ int ib_set_fields(ib_ctx* c, const double* u, const double* v, const double* w, 
             CKC(cudaMemsetAsync(sl->pstar, 0, fb, s->stream));
         }
     }
+    // X^n and U^{n-1} of the current time level (PAPER.md:686-697 restart from them)
+    CKC(undo_lookahead(s));
     CKC(cudaStreamSynchronize(s->stream));
+    clear_errors(s);
     s->step = 0;
-    s->ib_ahead = false;
     s->fields_set = true;
     return IB_OK;
 }
@@ -603,6 +668,7 @@ int ib_set_boundary(ib_ctx* c, int64_t npts, const double* X, int64_t nedges, co
     CKC(cudaStreamSynchronize(s->stream));
     drop_graphs(s);
     free_lagrangian(s);
+    clear_errors(s);
     s->step = 0;
     if (npts == 0) return IB_OK;
     const int d = s->dim;
@@ -800,6 +866,10 @@ int ib_step(ib_ctx* c, int64_t nsteps)
     Ctx* s = &c->s;
     if (!s->fields_set) return fail(IB_ESTATE, "ib_step before ib_set_fields");
     if (nsteps < 0) return fail(IB_EINVAL, "nsteps < 0");
+    {
+        const int pe = poll_errors(s);
+        if (pe != IB_OK) return pe;
+    }
     for (int64_t t = 0; t < nsteps; ++t) {
         const int first = (s->step == 0);
         if (!first && !s->profiling && s->use_graphs && !s->debug_keep_f) {
@@ -829,6 +899,7 @@ int ib_step(ib_ctx* c, int64_t nsteps)
         }
         swap_state(s);
         s->step++;
+        if (s->check_every > 0 && s->step % s->check_every == 0) CKC(enqueue_check(s));
         if (s->profiling) {
             CKC(cudaStreamSynchronize(s->stream));
             for (int ph = 0; ph < IB_NPHASES; ++ph) {
@@ -841,7 +912,7 @@ int ib_step(ib_ctx* c, int64_t nsteps)
             }
         }
     }
-    return IB_OK;
+    return poll_errors(s);
 }
 
 // all device work of one time step (Steps 1a-3f), enqueued on the context's stream
@@ -1045,6 +1116,14 @@ int ib_sync(ib_ctx* c)
 {
     if (!c) return fail(IB_EINVAL, "null context");
     CKC(cudaStreamSynchronize(c->s.stream));
+    return poll_errors(&c->s);
+}
+
+int ib_set_check_interval(ib_ctx* c, int64_t every)
+{
+    if (!c) return fail(IB_EINVAL, "null context");
+    if (every < 0) return fail(IB_EINVAL, "check interval must be >= 0");
+    c->s.check_every = every;
     return IB_OK;
 }
 
@@ -1070,6 +1149,126 @@ int ib_get_fields(ib_ctx* c, double* u, double* v, double* w, double* p, double*
     CKC(points_out(s, s->ib_ahead ? s->Xold : s->X, X));
     CKC(points_out(s, s->ib_ahead ? s->Uold : s->Uprev, U));
     CKC(cudaStreamSynchronize(s->stream));
+    return IB_OK;
+}
+
+// ---------------------------------------------------------------------------------
+// Checkpoint / resume: the complete state that the next step reads.
+// Blob = StateHdr, then per local slab u[d], G[d] (the momentum history N(u^{n-1}) +
+// (2/rho) f of a look-ahead), p, p* (nlocal doubles each), then the Lagrangian X, U^{n-1},
+// X_old, U_old ([npts][d] each, internal order) and the internal order pt_user[npts].
+// ---------------------------------------------------------------------------------
+struct StateHdr {
+    uint64_t magic;
+    int32_t version, dim;
+    int64_t n, nlocal_total, npts, step;
+    int32_t ib_ahead, nslabs, rank, nranks;
+    double dt, mu, rho, H;
+};
+static const uint64_t kStateMagic = 0x31564154534D4749ull;   // "IGMSTAV1"
+
+static int64_t state_bytes(Ctx* s)
+{
+    int64_t cells = 0;
+    for (int r = 0; r < nslabs(s); ++r) cells += slab_at(s, r)->nlocal;
+    return (int64_t)sizeof(StateHdr) + cells * (2 * s->dim + 2) * (int64_t)sizeof(double) +
+           s->npts * s->dim * 4 * (int64_t)sizeof(double) + s->npts * (int64_t)sizeof(int32_t);
+}
+
+int ib_state_size(ib_ctx* c, int64_t* bytes)
+{
+    if (!c || !bytes) return fail(IB_EINVAL, "null argument");
+    *bytes = state_bytes(&c->s);
+    return IB_OK;
+}
+
+int ib_get_state(ib_ctx* c, void* buf, int64_t bytes)
+{
+    if (!c || !buf) return fail(IB_EINVAL, "null argument");
+    Ctx* s = &c->s;
+    if (!s->fields_set) return fail(IB_ESTATE, "ib_get_state before ib_set_fields");
+    if (bytes < state_bytes(s)) return fail(IB_EINVAL, "state buffer of %lld bytes < %lld", (long long)bytes,
+                                            (long long)state_bytes(s));
+    StateHdr h;
+    memset(&h, 0, sizeof(h));
+    h.magic = kStateMagic; h.version = 1; h.dim = s->dim; h.n = s->n; h.npts = s->npts; h.step = s->step;
+    h.ib_ahead = s->ib_ahead ? 1 : 0; h.nslabs = nslabs(s);
+    h.rank = s->grp ? s->grp->rank : 0; h.nranks = s->grp ? s->grp->P : 1;
+    h.dt = s->dt; h.mu = s->mu; h.rho = s->rho; h.H = s->H;
+    for (int r = 0; r < nslabs(s); ++r) h.nlocal_total += slab_at(s, r)->nlocal;
+    memcpy(buf, &h, sizeof(h));
+    char* q = (char*)buf + sizeof(h);
+    for (int r = 0; r < nslabs(s); ++r) {
+        Ctx* sl = slab_at(s, r);
+        const size_t fb = (size_t)sl->nlocal * sizeof(double);
+        double* flds[8] = {sl->u[0], sl->u[1], sl->u[2], sl->nprev[0], sl->nprev[1], sl->nprev[2], sl->p, sl->pstar};
+        for (int k = 0; k < 8; ++k) {
+            if (k % 3 >= s->dim && k < 6) continue;
+            CKC(cudaMemcpyAsync(q, flds[k], fb, cudaMemcpyDeviceToHost, s->stream));
+            q += fb;
+        }
+    }
+    if (s->npts) {
+        const size_t pb = (size_t)s->npts * s->dim * sizeof(double);
+        double* lag[4] = {s->X, s->Uprev, s->Xold, s->Uold};
+        for (int k = 0; k < 4; ++k) { CKC(cudaMemcpyAsync(q, lag[k], pb, cudaMemcpyDeviceToHost, s->stream)); q += pb; }
+        CKC(cudaMemcpyAsync(q, s->pt_user, (size_t)s->npts * sizeof(int32_t), cudaMemcpyDeviceToHost, s->stream));
+    }
+    CKC(cudaStreamSynchronize(s->stream));
+    return poll_errors(s);
+}
+
+int ib_set_state(ib_ctx* c, const void* buf, int64_t bytes)
+{
+    if (!c || !buf) return fail(IB_EINVAL, "null argument");
+    Ctx* s = &c->s;
+    StateHdr h;
+    if (bytes < (int64_t)sizeof(h)) return fail(IB_EINVAL, "state buffer too small");
+    memcpy(&h, buf, sizeof(h));
+    int64_t cells = 0;
+    for (int r = 0; r < nslabs(s); ++r) cells += slab_at(s, r)->nlocal;
+    if (h.magic != kStateMagic || h.version != 1) return fail(IB_EINVAL, "not an ib_get_state blob");
+    if (h.dim != s->dim || h.n != s->n || h.nlocal_total != cells || h.nslabs != nslabs(s) ||
+        h.rank != (s->grp ? s->grp->rank : 0) || h.nranks != (s->grp ? s->grp->P : 1))
+        return fail(IB_EINVAL, "state blob is for another grid or decomposition");
+    if (h.dt != s->dt || h.mu != s->mu || h.rho != s->rho || h.H != s->H)
+        return fail(IB_EINVAL, "state blob is for other parameters (dt, mu, rho or H)");
+    if (h.npts != s->npts) return fail(IB_EINVAL, "state blob has %lld points, the context %lld (call ib_set_boundary "
+                                              "with the same boundary first)", (long long)h.npts, (long long)s->npts);
+    if (bytes < state_bytes(s)) return fail(IB_EINVAL, "state buffer truncated");
+    const char* q = (const char*)buf + sizeof(h);
+    if (s->npts) {
+        // the internal point order must be this context's (same boundary, same Morton order)
+        std::vector<int32_t> ord(s->npts);
+        const char* qo = q + (size_t)cells * (2 * s->dim + 2) * sizeof(double) + (size_t)s->npts * s->dim * 4 * sizeof(double);
+        CKC(cudaMemcpyAsync(ord.data(), s->pt_user, (size_t)s->npts * sizeof(int32_t), cudaMemcpyDeviceToHost, s->stream));
+        CKC(cudaStreamSynchronize(s->stream));
+        if (memcmp(ord.data(), qo, (size_t)s->npts * sizeof(int32_t)) != 0)
+            return fail(IB_EINVAL, "state blob was taken with another immersed boundary (point order differs)");
+    }
+    for (int r = 0; r < nslabs(s); ++r) {
+        Ctx* sl = slab_at(s, r);
+        const size_t fb = (size_t)sl->nlocal * sizeof(double);
+        double* flds[8] = {sl->u[0], sl->u[1], sl->u[2], sl->nprev[0], sl->nprev[1], sl->nprev[2], sl->p, sl->pstar};
+        for (int k = 0; k < 8; ++k) {
+            if (k % 3 >= s->dim && k < 6) continue;
+            CKC(cudaMemcpyAsync(flds[k], q, fb, cudaMemcpyHostToDevice, s->stream));
+            q += fb;
+        }
+    }
+    if (s->npts) {
+        const size_t pb = (size_t)s->npts * s->dim * sizeof(double);
+        double* lag[4] = {s->X, s->Uprev, s->Xold, s->Uold};
+        for (int k = 0; k < 4; ++k) { CKC(cudaMemcpyAsync(lag[k], q, pb, cudaMemcpyHostToDevice, s->stream)); q += pb; }
+        // (X^{n+1/2} and F are intermediates of an IB phase, not state: the next step
+        //  reads only G, X and U^{n-1})
+    }
+    // the blob may come from pinned memory the caller reuses right after the call
+    CKC(cudaStreamSynchronize(s->stream));
+    clear_errors(s);
+    s->step = h.step;
+    s->ib_ahead = h.ib_ahead != 0;
+    s->fields_set = true;
     return IB_OK;
 }
 
@@ -1194,7 +1393,8 @@ int ib_check_finite(ib_ctx* c)
     // nlocal is 0 when it holds no fields
     for (int r = 0; r <= (s->grp ? s->grp->nloc : 0); ++r) {
         Ctx* cc = (s->grp && r < s->grp->nloc) ? s->grp->slab[r] : s;
-        CKC(launch_check_finite(cc));
+        CKC(cudaMemsetAsync(cc->d_flag, 0, sizeof(int), s->stream));
+        CKC(launch_check_finite(cc, cc->d_flag));
         int flag = 0;
         CKC(cudaMemcpyAsync(&flag, cc->d_flag, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
         CKC(cudaStreamSynchronize(s->stream));
@@ -1204,9 +1404,12 @@ int ib_check_finite(ib_ctx* c)
     return IB_OK;
 }
 
-int ib_get_stats(ib_ctx* c, int64_t* launches, int64_t* steps)
+int ib_get_stats(ib_ctx* c, double* ms_per_phase, int64_t* steps, int64_t* launches)
 {
     if (!c) return fail(IB_EINVAL, "null context");
+    const Ctx* s = &c->s;
+    if (ms_per_phase)
+        for (int ph = 0; ph < IB_NPHASES; ++ph) ms_per_phase[ph] = s->ph_cnt[ph] ? s->ph_ms[ph] / s->ph_cnt[ph] : 0.0;
     if (launches) *launches = total_launches(&c->s);
     if (steps) *steps = c->s.step;
     return IB_OK;
@@ -1246,6 +1449,7 @@ int ib_destroy(ib_ctx* c)
     if (s->ev_fork) cudaEventDestroy(s->ev_fork);
     if (s->ev_join) cudaEventDestroy(s->ev_join);
     if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
+    if (s->err_h) cudaFreeHost(s->err_h);
     delete c;
     return IB_OK;
 }

@@ -171,7 +171,7 @@ template <int DIM>
 __global__ void k_force(const double* __restrict__ Xh, const int32_t* __restrict__ ptr,
                         const int32_t* __restrict__ nbr, const double* __restrict__ kap,
                         const double* __restrict__ rest, int has_rest, double* __restrict__ F, int64_t npts,
-                        double H, double invH)
+                        double H, double invH, int* __restrict__ err)
 {
     pdl_wait();
     pdl_trigger();
@@ -192,7 +192,17 @@ __global__ void k_force(const double* __restrict__ Xh, const int32_t* __restrict
         double t = kap[e];
         if (has_rest) {
             const double L = rest[e];
-            if (L != 0.0) t *= 1.0 - L / sqrt(l2);
+            if (L != 0.0) {
+                if (l2 > 0.0) {
+                    t *= 1.0 - L / sqrt(l2);
+                } else {
+                    // |X_m - X_k| = 0 with L != 0: the strain direction is undefined
+                    // (SPEC.md:140 singular strain).  Raise IB_EDEGENERATE and drop the
+                    // connection's (0-length) force instead of spreading NaN.
+                    *(volatile int*)(err + ERR_DEGENERATE) = 1;
+                    t = 0.0;
+                }
+            }
         }
 #pragma unroll
         for (int a = 0; a < DIM; ++a) acc[a] += t * d[a];
@@ -858,6 +868,9 @@ __global__ void __launch_bounds__(256) k_interp_quad(const double* __restrict__ 
     const int64_t kk = valid ? k : 0;
 #pragma unroll
     for (int a = 0; a < DIM; ++a) Xk[a] = X[kk * DIM + a];
+    // the DIM component groups of a point live in this block (blockDim is a multiple of
+    // 32 DIM), and each writes its component of X^{n+1} below: every read of X^n first
+    __syncthreads();
     int b[3];
     double w[3][4];
     quad_weights<DIM, KER>(Xk, c, invh, n, b, w);
@@ -1010,7 +1023,17 @@ __global__ void k_scatter_pts(const double* __restrict__ src, const int32_t* __r
 __global__ void k_check_finite(const double* __restrict__ a, size_t cnt, int* __restrict__ flag)
 {
     for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < cnt; q += (size_t)gridDim.x * blockDim.x)
-        if (!isfinite(a[q])) { atomicOr(flag, 1); return; }
+        if (!isfinite(a[q])) { *(volatile int*)flag = 1; return; }
+}
+
+// X^{n+1} - X^{n+1/2} = (X^{n+1} - X^n)/2: a point that moved more than one cell h in a
+// step (or a non-finite position) sets *flag (IB_EDOMAIN; "support stencil
+// exceeds resident+halo region")
+__global__ void k_check_domain(const double* __restrict__ X, const double* __restrict__ Xh, size_t cnt,
+                               double half_h, int* __restrict__ flag)
+{
+    for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < cnt; q += (size_t)gridDim.x * blockDim.x)
+        if (!(fabs(X[q] - Xh[q]) <= half_h)) { *(volatile int*)flag = 1; return; }
 }
 
 static unsigned nblk(int64_t cnt, int thr) { return (unsigned)((cnt + thr - 1) / thr); }
@@ -1038,10 +1061,14 @@ cudaError_t launch_interp_evolve(Ctx* s, int first)
     // 0.1954 -> 0.2009 ms/step)
     const int im = s->interp_mode ? s->interp_mode : (s->dim == 2 ? 3 : 4);
     if (im == 3) {
+        // a block holds whole 8-point groups of every component (32 DIM threads each):
+        // 256 threads in 2D, 192 in 3D, so the X^n reads of all components of a point
+        // precede its X^{n+1} writes (barrier in the kernel)
+        const int bs = s->dim == 3 ? 192 : 256;
         const int64_t thr = ((s->npts + 7) / 8) * 8 * s->dim * 4;
-        const unsigned nbk = (unsigned)((thr + 255) / 256);
+        const unsigned nbk = (unsigned)((thr + bs - 1) / bs);
         const double invh = 1.0 / s->h;
-#define IBGM_IQ(D, K) k_interp_quad<D, K><<<nbk, 256, 0, s->stream>>>(s->u[0], s->u[1], s->u[2], s->X, s->Xh, \
+#define IBGM_IQ(D, K) k_interp_quad<D, K><<<nbk, bs, 0, s->stream>>>(s->u[0], s->u[1], s->u[2], s->X, s->Xh, \
                                                                       s->Uprev, s->Xold, s->Uold, s->npts, (int)s->n, invh, \
                                                                       s->dt, first)
         if (s->dim == 2) { if (s->kernel == IB_DELTA_COS4) IBGM_IQ(2, 0); else IBGM_IQ(2, 1); }
@@ -1094,10 +1121,10 @@ cudaError_t launch_force(Ctx* s)
     const int thr = 128;
     if (s->dim == 2)
         launch_pdl_if(true, k_force<2>, dim3(nblk(s->npts, thr)), dim3(thr), 0, s->stream, s->Xh, s->csr_ptr, s->csr_nbr,
-                   s->csr_kappa, s->csr_rest, s->has_rest, s->F, s->npts, s->H, 1.0 / s->H);
+                   s->csr_kappa, s->csr_rest, s->has_rest, s->F, s->npts, s->H, 1.0 / s->H, s->err_d);
     else
         launch_pdl_if(false, k_force<3>, dim3(nblk(s->npts, thr)), dim3(thr), 0, s->stream, s->Xh, s->csr_ptr, s->csr_nbr,
-                   s->csr_kappa, s->csr_rest, s->has_rest, s->F, s->npts, s->H, 1.0 / s->H);
+                   s->csr_kappa, s->csr_rest, s->has_rest, s->F, s->npts, s->H, 1.0 / s->H, s->err_d);
     s->launches++;
     return cudaGetLastError();
 }
@@ -1256,21 +1283,30 @@ cudaError_t launch_spread(Ctx* s)
     return kp ? go_brick_spread<2, 1, kBrick2, true>(s) : go_brick_spread<2, 1, kBrick2, false>(s);
 }
 
-cudaError_t launch_check_finite(Ctx* s)
+cudaError_t launch_check_finite(Ctx* s, int* flag)
 {
     const int thr = 256;
-    cudaError_t e = cudaMemsetAsync(s->d_flag, 0, sizeof(int), s->stream);
-    if (e != cudaSuccess) return e;
-    for (int c = 0; c < s->dim; ++c) {
-        k_check_finite<<<592, thr, 0, s->stream>>>(s->u[c], (size_t)s->nlocal, s->d_flag);
+    if (s->nlocal > 0) {
+        for (int c = 0; c < s->dim; ++c) {
+            k_check_finite<<<592, thr, 0, s->stream>>>(s->u[c], (size_t)s->nlocal, flag);
+            s->launches++;
+        }
+        k_check_finite<<<592, thr, 0, s->stream>>>(s->p, (size_t)s->nlocal, flag);
         s->launches++;
     }
-    k_check_finite<<<592, thr, 0, s->stream>>>(s->p, (size_t)s->nlocal, s->d_flag);
-    s->launches++;
     if (s->npts) {
-        k_check_finite<<<592, thr, 0, s->stream>>>(s->X, (size_t)s->npts * s->dim, s->d_flag);
+        k_check_finite<<<592, thr, 0, s->stream>>>(s->X, (size_t)s->npts * s->dim, flag);
         s->launches++;
     }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_check_domain(Ctx* s, int* flag)
+{
+    if (s->npts == 0) return cudaSuccess;
+    k_check_domain<<<nblk(s->npts * s->dim, 256), 256, 0, s->stream>>>(s->X, s->Xh, (size_t)s->npts * s->dim,
+                                                                       0.5 * s->h, flag);
+    s->launches++;
     return cudaGetLastError();
 }
 

@@ -43,6 +43,9 @@ struct SchurInv {
 
 enum SysId { SYS_VISC = 0, SYS_PSI = 1, SYS_USER = 2, SYS_COUNT = 3 };
 
+// indices of the sticky error words (Ctx::err_h / err_d)
+enum ErrWord { ERR_NONFINITE = 0, ERR_DOMAIN = 1, ERR_DEGENERATE = 2, ERR_WORDS = 4 };
+
 struct Group;
 
 struct Ctx {
@@ -95,6 +98,12 @@ struct Ctx {
     bool fields_set;
     int64_t launches;
     int* d_flag;                      // device flag for finiteness checks
+    // sticky device-raised errors (mapped pinned host words, written by kernels with plain
+    // stores, read by the host without a synchronisation): ERR_* below.  Slabs share the
+    // top context's words.
+    int* err_h;
+    int* err_d;
+    int64_t check_every;              // in-step state check every K steps (0: off)
     // IB look-ahead: the IB phase of step n+1 (Steps 1-2, which need only u^{n+1} and X)
     // runs on a side stream concurrently with the psi passes of step n; ib_ahead says
     // it has been done, so X, Uprev, Xh, F and G already belong to the next step
@@ -243,7 +252,8 @@ cudaError_t launch_sub(Ctx* s, const double* a, const double* b, double* out);  
 cudaError_t launch_interp_evolve(Ctx* s, int first_step);    // Steps 1a-1c
 cudaError_t launch_force(Ctx* s);                            // Step 2a
 cudaError_t launch_spread(Ctx* s);                           // Step 2b (into G, and f in debug mode)
-cudaError_t launch_check_finite(Ctx* s);
+cudaError_t launch_check_finite(Ctx* s, int* flag);          // u, p (if held) and X non-finite -> *flag = 1
+cudaError_t launch_check_domain(Ctx* s, int* flag);          // a point moved > h in one step -> *flag = 1
 cudaError_t launch_scatter_pts(Ctx* s, const double* src, double* dst);   // internal -> caller order
 
 }  // namespace ibgm

@@ -42,7 +42,11 @@ _lib = None
 SYMBOLS = ["ib_default_options", "ib_create", "ib_set_fields", "ib_set_boundary", "ib_set_fibers",
            "ib_step", "ib_sync", "ib_get_fields", "ib_get_aux", "ib_line_solve", "ib_check_finite",
            "ib_get_stats", "ib_destroy", "ib_last_error", "ib_set_profiling", "ib_get_phase_times",
-           "ib_set_debug", "ib_nccl_unique_id", "ib_slab_range", "ib_psi_solve"]
+           "ib_set_debug", "ib_nccl_unique_id", "ib_slab_range", "ib_psi_solve", "ib_set_check_interval",
+           "ib_state_size", "ib_get_state", "ib_set_state"]
+
+IB_OK, IB_EINVAL, IB_ESTATE, IB_ECUDA, IB_ENCCL = 0, -1, -2, -3, -4
+IB_ENONFINITE, IB_EDOMAIN, IB_ENOMEM, IB_EDEGENERATE = -5, -6, -7, -8
 
 PHASES = ["interp_evolve", "force", "spread", "s1_rhs_xsweep", "sweep_y", "sweep_z", "div_psi_first",
           "psi_y", "psi_x_p", "clear"]
@@ -76,7 +80,11 @@ def lib():
         L.ib_get_aux.argtypes = [ctypes.c_void_p] + [_dp] * 8
         L.ib_line_solve.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_double, _dp, _dp]
         L.ib_check_finite.argtypes = [ctypes.c_void_p]
-        L.ib_get_stats.argtypes = [ctypes.c_void_p, _i64p, _i64p]
+        L.ib_get_stats.argtypes = [ctypes.c_void_p, _dp, _i64p, _i64p]
+        L.ib_set_check_interval.argtypes = [ctypes.c_void_p, ctypes.c_int64]
+        L.ib_state_size.argtypes = [ctypes.c_void_p, _i64p]
+        L.ib_get_state.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64]
+        L.ib_set_state.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64]
         L.ib_destroy.argtypes = [ctypes.c_void_p]
         L.ib_last_error.restype = ctypes.c_char_p
         L.ib_set_profiling.argtypes = [ctypes.c_void_p, ctypes.c_int32]
@@ -276,9 +284,34 @@ class Context:
         return {PHASES[i]: (float(ms[i]), int(cnt[i])) for i in range(len(PHASES)) if cnt[i] > 0}
 
     def stats(self):
+        ms = np.zeros(len(PHASES))
         a, b = ctypes.c_int64(), ctypes.c_int64()
-        _ck(lib().ib_get_stats(self._h, ctypes.byref(a), ctypes.byref(b)))
-        return dict(kernel_launches=a.value, steps=b.value)
+        _ck(lib().ib_get_stats(self._h, _p(ms), ctypes.byref(b), ctypes.byref(a)))
+        return dict(kernel_launches=a.value, steps=b.value,
+                    ms_per_phase={PHASES[i]: float(ms[i]) for i in range(len(PHASES)) if ms[i] > 0})
+
+    def set_check_interval(self, every: int):
+        _ck(lib().ib_set_check_interval(self._h, int(every)))
+
+    def state_size(self) -> int:
+        n = ctypes.c_int64()
+        _ck(lib().ib_state_size(self._h, ctypes.byref(n)))
+        return n.value
+
+    def get_state(self, buf=None):
+        """ib_get_state into `buf` (a writable uint8 buffer, e.g. pinned; allocated if None)."""
+        n = self.state_size()
+        if buf is None:
+            buf = np.empty(n, dtype=np.uint8)
+        if buf.nbytes < n or not buf.flags["C_CONTIGUOUS"]:
+            raise ValueError("state buffer too small or not contiguous")
+        _ck(lib().ib_get_state(self._h, ctypes.c_void_p(buf.ctypes.data), buf.nbytes))
+        return buf
+
+    def set_state(self, buf):
+        if not buf.flags["C_CONTIGUOUS"]:
+            raise ValueError("state buffer must be contiguous")
+        _ck(lib().ib_set_state(self._h, ctypes.c_void_p(buf.ctypes.data), buf.nbytes))
 
 
 def slab_of(a, nranks, rank):

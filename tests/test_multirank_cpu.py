@@ -63,3 +63,17 @@ def test_two_rank_gloo_host_logic(world, n):
         assert res[r]["ids_equal"] and res[r]["idlen"] == 128
         assert res[r]["reassembled"] and res[r]["local_ok"]
         assert res[r]["mx"] == float(world)                                # max over ranks
+
+
+def test_bench_gpus_n_relaunches_n_ranks():
+    """A bare `python bench.py --gpus 2` (no torchrun environment) starts two ranks under
+    torch.distributed.run with WORLD_SIZE=2 (--dry-run stops each rank before CUDA)."""
+    import json
+    import subprocess
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_PORT")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dry-run"],
+                       capture_output=True, text=True, env=env, timeout=300, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+    assert sorted(l["rank"] for l in lines) == [0, 1]
+    assert all(l["world_size"] == 2 and l["gpus"] == 2 for l in lines)
