@@ -253,6 +253,9 @@ __device__ __forceinline__ RowB row_bases(int j, int k, int n, int nl, int wrap)
 //   N_c = 1/(4h) sum_j [ (u_j(I+e_j) + u_j(I+e_j-e_c)) u_c(I+e_j) - (u_j(I) + u_j(I-e_c)) u_c(I-e_j) ]
 // L2 prefetch of the operands that miss in L1/L2 for cell i of a row (its centre, its
 // z-neighbour planes, the history G and p*), issued one row ahead by the fill loop
+#ifndef IBGM_S1_MINB
+#define IBGM_S1_MINB 4
+#endif
 #ifndef IBGM_S1_PREFETCH
 #define IBGM_S1_PREFETCH 1
 #endif
@@ -288,6 +291,43 @@ __device__ __forceinline__ void s1_prefetch(const S1Args& A, int i, const RowB& 
         pf_l2(A.G[c] + i + rb.r0);
     }
     pf_l2(A.pstar + i + rb.r0);
+}
+
+// The arithmetic of Steps 3a-3b at one cell from its gathered operands:
+//   U[m][q]  u_m at I, I+e_x, I-e_x, I+e_y, I-e_y, I+e_z, I-e_z   (q = 0, 1+2a, 2+2a)
+//   X[m][c]  u_m at I + e_m - e_c (m != c), the skew form's transport neighbours
+//   ps0, psm p* at I and I - e_c;  Gv the AB2 history G_c at I
+// returns N_c(u^n) and d_c = u*_c - u^n_c.
+template <int DIM>
+__device__ __forceinline__ void s1_eval(const S1Args& A, const double (&U)[DIM][1 + 2 * DIM],
+                                        const double (&X)[DIM][DIM], double ps0, const double (&psm)[3],
+                                        const double (&Gv)[3], double (&d)[3], double (&Nout)[3])
+{
+    const double invh = A.invh;
+    const double dt_rho = A.dt * A.inv_rho;
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) {
+        const double u0 = U[c][0];
+        double Nc = 0.0;
+        if (A.advection) {
+#pragma unroll
+            for (int jd = 0; jd < DIM; ++jd) {
+                const double Tp = U[jd][1 + 2 * jd] + ((jd == c) ? u0 : X[jd][c]);
+                const double Tm = U[jd][0] + U[jd][2 + 2 * c];
+                Nc = fma(Tp, U[c][1 + 2 * jd], Nc);
+                Nc = fma(-Tm, U[c][2 + 2 * jd], Nc);
+            }
+            Nc *= 0.25 * invh;
+        }
+        Nout[c] = Nc;
+        double lap = 0.0;
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) lap += U[c][1 + 2 * a] + U[c][2 + 2 * a];
+        lap = (lap - 2.0 * DIM * u0) * (invh * invh);
+        const double gp = A.first ? 0.0 : (ps0 - psm[c]) * invh;     // G^{C->E} p*
+        // u* - u^n = dt ( -3/2 N + 1/2 G + (mu lap - G p*)/rho ),  G carries f
+        d[c] = A.dt * (0.5 * Gv[c] - A.a1 * Nc) + dt_rho * (A.mu * lap - gp);
+    }
 }
 
 template <int DIM>
@@ -329,32 +369,13 @@ __device__ __forceinline__ void s1_cell(const S1Args& A, int i, const RowB& rb, 
 #pragma unroll
         for (int c = 0; c < DIM; ++c) psm[c] = ldg(A.pstar + o[2 + 2 * c]);
     }
-    const double invh = A.invh;
-    const double dt_rho = A.dt * A.inv_rho;
+    double Gv[3] = {0, 0, 0};
 #pragma unroll
-    for (int c = 0; c < DIM; ++c) {
-        const double u0 = U[c][0];
-        double Nc = 0.0;
-        if (A.advection) {
+    for (int c = 0; c < DIM; ++c) Gv[c] = ldg(A.G[c] + o[0]);
+    double Nv[3];
+    s1_eval<DIM>(A, U, X, ps0, psm, Gv, d, Nv);
 #pragma unroll
-            for (int jd = 0; jd < DIM; ++jd) {
-                const double Tp = U[jd][1 + 2 * jd] + ((jd == c) ? u0 : X[jd][c]);
-                const double Tm = U[jd][0] + U[jd][2 + 2 * c];
-                Nc = fma(Tp, U[c][1 + 2 * jd], Nc);
-                Nc = fma(-Tm, U[c][2 + 2 * jd], Nc);
-            }
-            Nc *= 0.25 * invh;
-        }
-        A.nadv[c][o[0]] = Nc;
-        double lap = 0.0;
-#pragma unroll
-        for (int a = 0; a < DIM; ++a) lap += U[c][1 + 2 * a] + U[c][2 + 2 * a];
-        lap = (lap - 2.0 * DIM * u0) * (invh * invh);
-        const double gp = A.first ? 0.0 : (ps0 - psm[c]) * invh;     // G^{C->E} p*
-        const double Gc = ldg(A.G[c] + o[0]);
-        // u* - u^n = dt ( -3/2 N + 1/2 G + (mu lap - G p*)/rho ),  G carries f
-        d[c] = A.dt * (0.5 * Gc - A.a1 * Nc) + dt_rho * (A.mu * lap - gp);
-    }
+    for (int c = 0; c < DIM; ++c) A.nadv[c][o[0]] = Nv[c];
 }
 
 // -------------------------------------------------------------------------------
@@ -623,6 +644,40 @@ __global__ void __launch_bounds__(256, MINB) k_lines(const LineCoef C, const Sch
 }
 
 // -------------------------------------------------------------------------------
+// Warp-independent x-line pass (S1, psi_x + Step 3f): every warp owns lpw = 32/P whole
+// x-lines in its own slice of shared memory and runs fill -> solve -> store with only
+// warp barriers, so the warps of an SM drift into different phases and the stencil
+// gathers of some overlap the register-resident solves of others (k_lines orders the
+// three phases of all its warps with block barriers: the memory system idles while
+// the whole block solves).
+// -------------------------------------------------------------------------------
+template <int L, int KIND, int DIM, int NC, int WPB, int MINB>
+__global__ void __launch_bounds__(32 * WPB, MINB) k_xwarp(const LineCoef C, const SchurInv* __restrict__ SI, int n,
+                                                          LArgs A)
+{
+    using LP = LinePass<L, KIND, DIM, 0, NC>;
+    extern __shared__ double smem[];
+    const int P = C.P;
+    const int TP = tile_pitch(P, L);
+    const int lpw = 32 / P;
+    constexpr int NT = (KIND == K_PSI_LAST) ? 2 : 1;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double* sinvT = smem;
+    double* tile = smem + P * P + (size_t)w * NT * NC * lpw * TP;
+    double* tile2 = tile + (size_t)NC * lpw * TP;
+    load_sinvT(sinvT, SI, P);
+    __syncthreads();
+    const int g0 = (blockIdx.x * WPB + w) * lpw;
+    const int nrow = (DIM == 2) ? A.nl : n;
+    if (g0 >= nrow) return;
+    LP::fill(tile, tile2, A, n, lpw, TP, g0, blockIdx.y, 0, lane, 32);
+    __syncwarp();
+    LP::solve(tile, C, sinvT, lpw, TP, 0, 1);
+    __syncwarp();
+    LP::store(tile, tile2, A, n, lpw, TP, g0, blockIdx.y, 0, lane, 32);
+}
+
+// -------------------------------------------------------------------------------
 // Strided-line pass (y / z lines, and y in 2D): one thread per (line, part).  A block
 // holds RI neighbouring lines (consecutive i) x P parts; warp w covers RI lines of one
 // part, so each of a thread's L loads is one coalesced RI-wide row.  The part stays in
@@ -767,6 +822,17 @@ bool pdl_enabled()
     return v == 1;
 }
 
+// x-line passes by k_xwarp (IBGM_XWARP=0: the block-tiled k_lines pass, for A/B)
+static bool xwarp_enabled()
+{
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("IBGM_XWARP");
+        v = (e && atoi(e) == 0) ? 0 : 1;
+    }
+    return v == 1;
+}
+
 static int sm_count()
 {
     static int n = 0;
@@ -861,6 +927,27 @@ static cudaError_t go_lines(Ctx* s, int sys, const LArgs& a, int ncomp_grid)
     }
     const int64_t rows = (AX == 0 && DIM == 2) ? s->nl : s->n;
     const int gy = (DIM == 3) ? (int)s->nl : 1;
+    if constexpr (AX == 0 && L <= kMaxL && (KIND == K_S1 || KIND == K_PSI_LAST)) {
+        // measured (graph ms/step): config 4 (384^3) 5.056 -> 4.957; config 3 (128^3) 0.1686 ->
+        // 0.1724 and config 2 (1024^2) 0.066 -> 0.075 slower, so only 3D grids of N >= 256
+        if (xwarp_enabled() && DIM == 3 && s->n >= 256 && s->P <= 32) {
+            constexpr int WPB = 4;
+            constexpr int MINB = (KIND == K_S1) ? IBGM_S1_MINB : 8;
+            auto kern = k_xwarp<L, KIND, DIM, NC, WPB, MINB>;
+            const int lpw = 32 / s->P;
+            const int TP = tile_pitch(s->P, L);
+            const int NT = (KIND == K_PSI_LAST) ? 2 : 1;
+            const size_t sm = ((size_t)s->P * s->P + (size_t)WPB * NT * NC * lpw * TP) * sizeof(double);
+            static unsigned long long attr_mask = 0;
+            const cudaError_t ae = smem_attr_once(attr_mask, kern, (int)smem_limit());
+            if (ae != cudaSuccess) return ae;
+            la.s1flat = 1;
+            const dim3 grid((unsigned)((rows + WPB * lpw - 1) / (WPB * lpw)), (unsigned)gy, 1u);
+            kern<<<grid, 32 * WPB, sm, s->stream>>>(s->hcoef[sys], s->sinv + sys, (int)s->n, la);
+            s->launches++;
+            return cudaGetLastError();
+        }
+    }
     return go_lines_k<L, KIND, DIM, AX, NC, (KIND == K_S1 || L >= 24) ? 2 : 4>(s, sys, la, ncomp_grid, rows, gy);
 }
 
