@@ -520,14 +520,6 @@ int ib_create(const ib_grid* grid, double nu, double rho, double dt, const ib_op
         s->nlocal = s->ncell;
         s->hoff = 0;
         CKC(alloc_fields(s));
-        // the look-ahead IB kernels (latency-bound, few blocks) get the higher priority so
-        // that their blocks take SM slots as the psi passes' blocks retire
-        int prio_lo = 0, prio_hi = 0;
-        CKC(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
-        CKC(cudaStreamCreateWithPriority(&s->side, cudaStreamNonBlocking, prio_hi));
-        CKC(cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming));
-        CKC(cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming));
-        s->lookahead = 1;
     } else {
         // z-slab decomposition: the top context keeps the Lagrangian state; each slab
         // context holds the fields of nz planes (+ halos) and borrows the stream and the
@@ -573,25 +565,36 @@ int ib_create(const ib_grid* grid, double nu, double rho, double dt, const ib_op
         }
         // (Q stays 1 when one part per slab already gives enough threads: every extra
         //  part adds one reduced-system row per line to the master exchange)
+        // parts of at most 17 planes keep the forward phase's column in registers
+        // (k_slab_fwd_reg: one read of d and one write of f* per cell, against the two
+        // passes of k_slab_fwd), at Q + 2 more scalars per line in the exchange
+        while (nz / G->Q > 17 && G->Q < nz && (G->Q + 1) * P <= kSlabMaxParts) {
+            ++G->Q;
+            while (G->Q < nz && nz % G->Q != 0) ++G->Q;
+        }
+        {
+            const char* e = getenv("IBGM_SLAB_Q");   // A/B override
+            if (e && atoi(e) > 0 && nz % atoi(e) == 0) G->Q = atoi(e);
+        }
         if (nz / G->Q < 2) G->Q = nz / 2;
         if (G->Q * P > kSlabMaxParts) G->Q = kSlabMaxParts / P > 0 ? kSlabMaxParts / P : 1;   // reduced system <= kSlabMaxParts
         if (G->Q < 1) G->Q = 1;
         while (nz % G->Q != 0) --G->Q;
         {
-            // exchange buffers (slab.cu): EMULATE keeps one shared UP / DN, NCCL a send and
-            // a receive buffer each
+            // exchange buffers (slab.cu layouts): a send and a receive buffer per rank; the
+            // EMULATE context holds the P ranks' sets back to back
             const size_t NI = (size_t)(s->plane / P), nb = (size_t)G->Q + 2;
             const bool emu = (o.transport == IB_TRANSPORT_EMULATE);
             const size_t up = (size_t)P * G->Q * kSlabSlots * NI * (emu ? P : 1);
             const size_t dn = (size_t)P * 3 * nb * NI * (emu ? P : 1);
             CKC(cudaMalloc(&G->up_s, up * sizeof(double)));
             CKC(cudaMalloc(&G->dn_s, dn * sizeof(double)));
+            CKC(cudaMalloc(&G->up_rv, up * sizeof(double)));
+            CKC(cudaMalloc(&G->dn_rv, dn * sizeof(double)));
             CKC(cudaMemsetAsync(G->up_s, 0, up * sizeof(double), s->stream));
             CKC(cudaMemsetAsync(G->dn_s, 0, dn * sizeof(double), s->stream));
-            if (!emu) {
-                CKC(cudaMalloc(&G->up_rv, up * sizeof(double)));
-                CKC(cudaMalloc(&G->dn_rv, dn * sizeof(double)));
-            }
+            CKC(cudaMemsetAsync(G->up_rv, 0, up * sizeof(double), s->stream));
+            CKC(cudaMemsetAsync(G->dn_rv, 0, dn * sizeof(double), s->stream));
         }
         int rc;
         if ((rc = upload_coef(s, SYS_VISC, -kv, 1.0 + 2.0 * kv, -kv, 0)) != IB_OK) return rc;
@@ -603,7 +606,19 @@ int ib_create(const ib_grid* grid, double nu, double rho, double dt, const ib_op
             memcpy(&id, o.nccl_id, sizeof(id));
             const int nr = nccl_comm_init(&G->comm, P, &id, o.rank);
             if (nr != 0) return fail(IB_ENCCL, "ncclCommInitRank: %s", nccl_error_string(nr));
+            // (collective; without ncclCommSplit the slab look-ahead stays off)
+            if (nccl_comm_split(G->comm, o.rank, &G->comm_side) != 0) G->comm_side = nullptr;
         }
+    }
+    {
+        // the look-ahead IB kernels (latency-bound, few blocks) get the higher priority so
+        // that their blocks take SM slots as the psi passes' blocks retire
+        int prio_lo = 0, prio_hi = 0;
+        CKC(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+        CKC(cudaStreamCreateWithPriority(&s->side, cudaStreamNonBlocking, prio_hi));
+        CKC(cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming));
+        CKC(cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming));
+        s->lookahead = 1;
     }
     // brick grid for the binned spread: 4^3 cells (3D) / 8^2 (2D)
     {
@@ -848,7 +863,9 @@ static int enqueue_any(Ctx* s, int first) { return s->grp ? enqueue_step_slab(s,
 
 static bool lookahead_on(const Ctx* s)
 {
-    return s->lookahead && !s->grp && s->npts > 0 && !s->profiling && !s->debug_keep_f;
+    // on z-slabs the look-ahead's all-reduce of U needs its own communicator (NCCL)
+    const bool slab_ok = !s->grp || s->grp->transport == IB_TRANSPORT_EMULATE || s->grp->comm_side != nullptr;
+    return s->lookahead && slab_ok && s->npts > 0 && !s->profiling && !s->debug_keep_f;
 }
 
 // Steps 1-2 (interpolate + evolve, force, spread) on context view v
@@ -973,34 +990,54 @@ static double* fld_st_last3(Ctx* c) { return c->st[2]; }
 // The same step on a z-slab decomposition: each phase runs on every local slab, with
 // the exchanges between phases (a12: halos, a13: the cut-axis line solves, and the
 // sum of the partial interpolations).
+// Steps 1-2 on a z-slab decomposition (top: the context holding the Lagrangian state,
+// views: its slabs, all possibly re-pointed for the look-ahead; side: the all-reduce
+// runs on the look-ahead communicator)
+static int enqueue_ib_slab(Ctx* s, Ctx* top, Ctx* const* views, int first, bool side)
+{
+    Group* G = s->grp;
+    const int d = s->dim;
+    if (s->profiling) CKC(cudaEventRecord(s->ev[IB_PH_INTERP][0], top->stream));
+    // Step 1a: each slab interpolates from the nodes it owns; U^n = sum over slabs
+    const int64_t cnt = top->npts * d;
+    for (int r = 0; r < G->nloc; ++r) {
+        double* part = G->Upart + ((G->transport == IB_TRANSPORT_EMULATE) ? (size_t)r * cnt : 0);
+        CKC(slab_interp_part(top, views[r], part, G->sel[r], G->sel_cnt + r));
+    }
+    CKG(group_allreduce_U(G, top, top->stream, side));
+    // Steps 1b-1c on every rank (identical arithmetic on identical U^n)
+    CKC(slab_evolve(top, G->Ured, first));
+    if (s->profiling) {
+        CKC(cudaEventRecord(s->ev[IB_PH_INTERP][1], top->stream));
+        s->ph_pending[IB_PH_INTERP] = true;
+    }
+    if (s->profiling) CKC(cudaEventRecord(s->ev[IB_PH_FORCE][0], top->stream));
+    CKC(launch_force(top));
+    if (s->profiling) {
+        CKC(cudaEventRecord(s->ev[IB_PH_FORCE][1], top->stream));
+        s->ph_pending[IB_PH_FORCE] = true;
+    }
+    if (s->profiling) CKC(cudaEventRecord(s->ev[IB_PH_SPREAD][0], top->stream));
+    for (int r = 0; r < G->nloc; ++r) CKC(slab_spread_part(top, views[r], G->sel[r], G->sel_cnt + r));
+    if (s->profiling) {
+        CKC(cudaEventRecord(s->ev[IB_PH_SPREAD][1], top->stream));
+        s->ph_pending[IB_PH_SPREAD] = true;
+    }
+    return IB_OK;
+}
+
+// The same step on a z-slab decomposition: each phase runs on every local slab, with
+// the exchanges between phases (a12: halos, a13: the cut-axis line solves, and the
+// sum of the partial interpolations).
 static int enqueue_step_slab(Ctx* s, int first)
 {
     const int d = s->dim;
     Group* G = s->grp;
     if (first) FOR_SLABS(clear3(sl, sl->nprev));
     if (s->debug_keep_f && s->npts > 0) FOR_SLABS(clear3(sl, sl->f));
-    if (s->npts > 0) {
-        if (s->profiling) CKC(cudaEventRecord(s->ev[IB_PH_INTERP][0], s->stream));
-        // Step 1a: each slab interpolates from the nodes it owns; U^n = sum over slabs
-        const int64_t cnt = s->npts * d;
-        for (int r = 0; r < G->nloc; ++r) {
-            double* part = G->Upart + ((G->transport == IB_TRANSPORT_EMULATE) ? (size_t)r * cnt : 0);
-            CKC(slab_interp_part(s, G->slab[r], part, G->sel[r], G->sel_cnt + r));
-        }
-        CKG(group_allreduce_U(G, s, s->stream));
-        // Steps 1b-1c on every rank (identical arithmetic on identical U^n)
-        CKC(slab_evolve(s, G->Ured, first));
-        if (s->profiling) {
-            CKC(cudaEventRecord(s->ev[IB_PH_INTERP][1], s->stream));
-            s->ph_pending[IB_PH_INTERP] = true;
-        }
-        PHASE(IB_PH_FORCE, launch_force(s));
-        if (s->profiling) CKC(cudaEventRecord(s->ev[IB_PH_SPREAD][0], s->stream));
-        for (int r = 0; r < G->nloc; ++r) CKC(slab_spread_part(s, G->slab[r], G->sel[r], G->sel_cnt + r));
-        if (s->profiling) {
-            CKC(cudaEventRecord(s->ev[IB_PH_SPREAD][1], s->stream));
-            s->ph_pending[IB_PH_SPREAD] = true;
-        }
+    if (s->npts > 0 && !s->ib_ahead) {
+        const int rc = enqueue_ib_slab(s, s, G->slab, first, false);
+        if (rc != IB_OK) return rc;
     }
     if (s->profiling) CKC(cudaEventRecord(s->ev[IB_PH_S1][0], s->stream));
     // halos for Steps 3a-3b: u (every component) on both sides, p* below
@@ -1034,6 +1071,31 @@ static int enqueue_step_slab(Ctx* s, int first)
         CKC(cudaEventRecord(s->ev[last_ph][1], s->stream));
         s->ph_pending[last_ph] = true;
     }
+    // look-ahead (as on one GPU): Steps 1-2 of step n+1 need u^{n+1} (now in st, owned
+    // planes only), X and U^n; on the side stream, spreading into N(u^n) = the next
+    // step's history, while the psi passes below run
+    const bool look = lookahead_on(s);
+    Ctx vtop = *s;
+    std::vector<Ctx> vsl(look ? G->nloc : 0);
+    Ctx* vptr[kMaxRanks];
+    if (look) {
+        vtop.stream = s->side;
+        vtop.launches = 0;
+        for (int r = 0; r < G->nloc; ++r) {
+            vsl[r] = *G->slab[r];
+            for (int q = 0; q < 3; ++q) { vsl[r].u[q] = G->slab[r]->st[q]; vsl[r].nprev[q] = G->slab[r]->nadv[q]; }
+            vsl[r].stream = s->side;
+            vsl[r].launches = 0;
+            vptr[r] = &vsl[r];
+        }
+        CKC(cudaEventRecord(s->ev_fork, s->stream));
+        CKC(cudaStreamWaitEvent(s->side, s->ev_fork, 0));
+        const int rc = enqueue_ib_slab(s, &vtop, vptr, 0, true);
+        if (rc != IB_OK) return rc;
+        CKC(cudaEventRecord(s->ev_join, s->side));
+        s->launches += vtop.launches;
+        for (int r = 0; r < G->nloc; ++r) s->launches += vsl[r].launches;
+    }
     // Step 3e: D.u^{n+1} needs u^{n+1}_last one plane above
     if (s->profiling) CKC(cudaEventRecord(s->ev[IB_PH_DIVPSI][0], s->stream));
     {
@@ -1063,6 +1125,8 @@ static int enqueue_step_slab(Ctx* s, int first)
         CKC(cudaEventRecord(s->ev[IB_PH_PSI_X][1], s->stream));
         s->ph_pending[IB_PH_PSI_X] = true;
     }
+    if (look) CKC(cudaStreamWaitEvent(s->stream, s->ev_join, 0));
+    s->ib_ahead = look;
     return IB_OK;
 }
 
@@ -1431,6 +1495,7 @@ int ib_destroy(ib_ctx* c)
         cudaFree(G->up_s); cudaFree(G->up_rv); cudaFree(G->dn_s); cudaFree(G->dn_rv);
         for (int k = 0; k < SYS_COUNT; ++k) cudaFree(G->coef[k]);
         free_lagrangian(s);
+        nccl_comm_destroy(G->comm_side);
         nccl_comm_destroy(G->comm);
         delete G;
         s->grp = nullptr;

@@ -916,13 +916,18 @@ __global__ void __launch_bounds__(256) k_interp_quad(const double* __restrict__ 
     Uold[k * DIM + c] = up;
 }
 
-template <int DIM, int KER, bool KEEP>
+// PART (z-slab, slab.cu): the items are the `*count` points of `list` whose support meets
+// this slab's planes z0 .. z0+nzl-1 of the last axis, and only rows inside the slab are
+// accumulated (into the slab's fields, addressed by local plane).
+template <int DIM, int KER, bool KEEP, bool PART>
 __global__ void __launch_bounds__(256) k_spread_quad(const double* __restrict__ Xh, const double* __restrict__ F,
                                                      const double* __restrict__ wgt, double* __restrict__ g0,
                                                      double* __restrict__ g1, double* __restrict__ g2,
                                                      double* __restrict__ f0, double* __restrict__ f1,
                                                      double* __restrict__ f2, int64_t npts, int n, double invh,
-                                                     double invhd, double two_rho, int red)
+                                                     double invhd, double two_rho, int red,
+                                                     const int* __restrict__ list, const int* __restrict__ count,
+                                                     int z0, int nzl)
 {
     pdl_wait();
     pdl_trigger();
@@ -931,10 +936,13 @@ __global__ void __launch_bounds__(256) k_spread_quad(const double* __restrict__ 
     const int64_t blk = g / (8 * DIM);
     const int rem = (int)(g - blk * 8 * DIM);
     const int c = rem >> 3;
-    int64_t k = blk * 8 + (rem & 7);
-    const bool valid = k < npts;
+    const int64_t item = blk * 8 + (rem & 7);
+    const int64_t nitem = PART ? (int64_t)*count : npts;
+    const bool valid = item < nitem;
+    if (PART && blk * 8 >= nitem) return;  // the whole warp is past the list
     if (!red && !valid) return;
-    if (!valid) k = npts - 1;              // red: every lane takes part in the shuffles
+    int64_t k = valid ? item : nitem - 1;  // red: every lane takes part in the shuffles
+    if (PART) k = list[k];
     double Xk[3] = {0, 0, 0};
 #pragma unroll
     for (int a = 0; a < DIM; ++a) Xk[a] = Xh[k * DIM + a];
@@ -984,9 +992,10 @@ __global__ void __launch_bounds__(256) k_spread_quad(const double* __restrict__ 
             int iy = b[1] + m1;
             if (iy >= n) iy -= n;
             const double v = reduce(Fx * w[1][m1]);
-            if (head) {
-                atomicAdd(gc + nn * iy + ix, two_rho * v);
-                if (KEEP) atomicAdd(fc + nn * iy + ix, v);
+            const int ly = PART ? iy - z0 : iy;
+            if (head && (!PART || (unsigned)ly < (unsigned)nzl)) {
+                atomicAdd(gc + nn * ly + ix, two_rho * v);
+                if (KEEP) atomicAdd(fc + nn * ly + ix, v);
             }
         }
     } else {
@@ -994,20 +1003,109 @@ __global__ void __launch_bounds__(256) k_spread_quad(const double* __restrict__ 
         for (int m2 = 0; m2 < 4; ++m2) {
             int iz = b[2] + m2;
             if (iz >= n) iz -= n;
+            const int lz = PART ? iz - z0 : iz;
+            const bool in = !PART || (unsigned)lz < (unsigned)nzl;
             const double a2 = Fx * w[2][m2];
 #pragma unroll
             for (int m1 = 0; m1 < 4; ++m1) {
                 int iy = b[1] + m1;
                 if (iy >= n) iy -= n;
                 const double v = reduce(a2 * w[1][m1]);
-                const size_t q = nn * (nn * iz + iy) + ix;
-                if (head) {
+                const size_t q = nn * (nn * (size_t)(in ? lz : 0) + iy) + ix;
+                if (head && in) {
                     atomicAdd(gc + q, two_rho * v);
                     if (KEEP) atomicAdd(fc + q, v);
                 }
             }
         }
     }
+}
+
+// Step 1a restricted to the nodes of one z-slab (slab.cu): one thread per (listed point,
+// component), 64 points per 64*DIM block; the partial sums over ranks form U^n.
+template <int DIM, int KER>
+__global__ void __launch_bounds__(64 * DIM) k_interp_comp_part(const double* __restrict__ u0,
+                                                             const double* __restrict__ u1,
+                                                             const double* __restrict__ u2,
+                                                             const double* __restrict__ X, double* __restrict__ Upart,
+                                                             const int* __restrict__ list,
+                                                             const int* __restrict__ count, int n, int z0, int nzl,
+                                                             double invh)
+{
+    const int c = threadIdx.x >> 6;
+    const int64_t i = blockIdx.x * 64LL + (threadIdx.x & 63);
+    if (i >= *count) return;
+    const int64_t k = list[i];
+    const double* uc = (c == 0) ? u0 : (c == 1 ? u1 : u2);
+    const size_t nn = (size_t)n;
+    int b[3] = {0, 0, 0};
+    double w[3][4];
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) {
+        weights4u<KER>(X[k * DIM + a] * invh - (a == c ? 0.0 : 0.5), b[a], w[a]);
+        b[a] = wrapm(b[a], n);
+    }
+    double acc = 0.0;
+#pragma unroll
+    for (int mL = 0; mL < 4; ++mL) {
+        int iL = b[DIM - 1] + mL;
+        if (iL >= n) iL -= n;
+        const int l = iL - z0;
+        if ((unsigned)l >= (unsigned)nzl) continue;
+        double pa = 0.0;
+        if (DIM == 2) {
+#pragma unroll
+            for (int m0 = 0; m0 < 4; ++m0) pa += w[0][m0] * __ldg(uc + nn * l + wrap1(b[0] + m0, n));
+        } else {
+#pragma unroll
+            for (int m1 = 0; m1 < 4; ++m1) {
+                const size_t row = nn * (nn * (size_t)l + (size_t)wrap1(b[1] + m1, n));
+                double r = 0.0;
+#pragma unroll
+                for (int m0 = 0; m0 < 4; ++m0) r += w[0][m0] * __ldg(uc + row + wrap1(b[0] + m0, n));
+                pa += w[1][m1] * r;
+            }
+        }
+        acc += w[DIM - 1][mL] * pa;
+    }
+    Upart[k * DIM + c] = acc;
+}
+
+cudaError_t launch_interp_part(Ctx* top, Ctx* s, double* Upart, const int* list, const int* count)
+{
+    const unsigned nb = (unsigned)((top->npts + 63) / 64);
+    const double invh = 1.0 / s->h;
+#define IBGM_ICP(D, K) k_interp_comp_part<D, K><<<nb, 64 * D, 0, s->stream>>>(s->u[0], s->u[1], s->u[2], top->X, Upart, \
+        list, count, (int)s->n, (int)s->z0, (int)s->nl, invh)
+    if (s->dim == 2) { if (top->kernel == IB_DELTA_COS4) IBGM_ICP(2, 0); else IBGM_ICP(2, 1); }
+    else { if (top->kernel == IB_DELTA_COS4) IBGM_ICP(3, 0); else IBGM_ICP(3, 1); }
+#undef IBGM_ICP
+    s->launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_spread_part(Ctx* top, Ctx* s, const int* list, const int* count)
+{
+    const int64_t thr = ((top->npts + 7) / 8) * 8 * s->dim * 4;
+    const unsigned nbk = (unsigned)((thr + 255) / 256);
+    const double invh = 1.0 / s->h;
+    const double invhd = (s->dim == 3) ? invh * invh * invh : invh * invh;
+    const double two_rho = 2.0 / s->rho;
+    const int red = (s->dim == 3) ? 1 : 0;
+#define IBGM_SQP(D, K, KP) k_spread_quad<D, K, KP, true><<<nbk, 256, 0, s->stream>>>(top->Xh, top->F, top->wgt, \
+        s->nprev[0], s->nprev[1], s->nprev[2], s->f[0], s->f[1], s->f[2], top->npts, (int)s->n, invh, invhd, two_rho, \
+        red, list, count, (int)s->z0, (int)s->nl)
+    const bool kp = top->debug_keep_f != 0;
+    if (s->dim == 2) {
+        if (top->kernel == IB_DELTA_COS4) { if (kp) IBGM_SQP(2, 0, true); else IBGM_SQP(2, 0, false); }
+        else { if (kp) IBGM_SQP(2, 1, true); else IBGM_SQP(2, 1, false); }
+    } else {
+        if (top->kernel == IB_DELTA_COS4) { if (kp) IBGM_SQP(3, 0, true); else IBGM_SQP(3, 0, false); }
+        else { if (kp) IBGM_SQP(3, 1, true); else IBGM_SQP(3, 1, false); }
+    }
+#undef IBGM_SQP
+    s->launches++;
+    return cudaGetLastError();
 }
 
 // dst[idx[i]] = src[i] per point (internal -> caller order)
@@ -1229,9 +1327,9 @@ static cudaError_t launch_spread_quad(Ctx* s)
     // auto: with the warp pre-reduction in 3D (config 4 spread 460 -> 348 us, config 3
     // 30.3 -> 24.9 us), without in 2D (no runs of equal base nodes on a curve: no gain)
     const int red = (s->spread_mode == 5 || (s->spread_mode == 0 && s->dim == 3)) ? 1 : 0;
-#define IBGM_SQ(D, K, KP) launch_pdl_if(D == 2, k_spread_quad<D, K, KP>, dim3(nbk), dim3(256), 0, s->stream, s->Xh, s->F, \
-        s->wgt, s->nprev[0], s->nprev[1], s->nprev[2], s->f[0], s->f[1], s->f[2], s->npts, (int)s->n, invh, invhd, \
-        two_rho, red)
+#define IBGM_SQ(D, K, KP) launch_pdl_if(D == 2, k_spread_quad<D, K, KP, false>, dim3(nbk), dim3(256), 0, s->stream, s->Xh, \
+        s->F, s->wgt, s->nprev[0], s->nprev[1], s->nprev[2], s->f[0], s->f[1], s->f[2], s->npts, (int)s->n, invh, invhd, \
+        two_rho, red, (const int*)nullptr, (const int*)nullptr, 0, 0)
     const bool kp = s->debug_keep_f != 0;
     if (s->dim == 2) {
         if (s->kernel == IB_DELTA_COS4) { if (kp) IBGM_SQ(2, 0, true); else IBGM_SQ(2, 0, false); }

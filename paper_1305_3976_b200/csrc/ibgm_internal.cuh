@@ -155,6 +155,8 @@ struct Group {
     int* sel_cnt;                     // [nloc] counters
     double* coef[SYS_COUNT];          // device slab coefficient blocks
     void* comm;                       // ncclComm_t
+    void* comm_side;                  // a second communicator (ncclCommSplit) for the IB
+                                      // look-ahead's all-reduce on the side stream
 };
 
 struct HaloSpec {
@@ -176,13 +178,14 @@ cudaError_t slab_user_fwd(Ctx* s, Group* G, double* data, int mf);
 cudaError_t slab_user_corr(Ctx* s, Group* G, double* data, int mf);
 cudaError_t slab_interp_part(Ctx* top, Ctx* s, double* Upart, int* list, int* count);
 cudaError_t slab_sum_slots(Ctx* top, const double* part, int P, double* out);
-cudaError_t slab_evolve(Ctx* top, const double* U, int first);
+cudaError_t slab_evolve(Ctx* top, const double* U, int first);   // also keeps X^n, U^{n-1} in Xold, Uold
 cudaError_t slab_spread_part(Ctx* top, Ctx* s, int* list, int* count);
 int group_halo(Group* G, int nf, const HaloSpec* spec, cudaStream_t st);
 int group_up(Group* G, int ns, cudaStream_t st);          // scalars to the line masters
 int group_dn(Group* G, int ncomp, cudaStream_t st);       // y and corrections back
 cudaError_t slab_master(Ctx* s, Group* G, int sys, int ncomp, int ns, int mf);
-int group_allreduce_U(Group* G, Ctx* top, cudaStream_t st);
+int group_allreduce_U(Group* G, Ctx* top, cudaStream_t st, bool side = false);
+int nccl_comm_split(void* comm, int rank, void** out);      // ncclCommSplit (0 ok; -1 unavailable)
 
 // ---------------------------------------------------------------------------------
 // Programmatic dependent launch: a kernel launched with launch_pdl may become resident
@@ -255,5 +258,8 @@ cudaError_t launch_spread(Ctx* s);                           // Step 2b (into G,
 cudaError_t launch_check_finite(Ctx* s, int* flag);          // u, p (if held) and X non-finite -> *flag = 1
 cudaError_t launch_check_domain(Ctx* s, int* flag);          // a point moved > h in one step -> *flag = 1
 cudaError_t launch_scatter_pts(Ctx* s, const double* src, double* dst);   // internal -> caller order
+// z-slab IB (slab.cu calls): the listed points, restricted to slab s's planes
+cudaError_t launch_interp_part(Ctx* top, Ctx* s, double* Upart, const int* list, const int* count);
+cudaError_t launch_spread_part(Ctx* top, Ctx* s, const int* list, const int* count);
 
 }  // namespace ibgm

@@ -34,6 +34,8 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <algorithm>
+
 #include "ibgm_internal.cuh"
 
 namespace ibgm {
@@ -50,6 +52,7 @@ struct NcclApi {
     int (*AllGather)(const void*, void*, size_t, int, void*, cudaStream_t) = nullptr;
     int (*Send)(const void*, size_t, int, int, void*, cudaStream_t) = nullptr;
     int (*Recv)(void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+    int (*CommSplit)(void*, int, int, void**, void*) = nullptr;   // optional (NCCL >= 2.18)
     int (*GroupStart)() = nullptr;
     int (*GroupEnd)() = nullptr;
     const char* (*GetErrorString)(int) = nullptr;
@@ -89,6 +92,7 @@ const char* nccl_load(void)
     IBGM_SYM(GroupEnd, "ncclGroupEnd");
     IBGM_SYM(GetErrorString, "ncclGetErrorString");
 #undef IBGM_SYM
+    g_nccl.CommSplit = reinterpret_cast<decltype(g_nccl.CommSplit)>(dlsym(h, "ncclCommSplit"));
     g_nccl.ok = true;
     return nullptr;
 }
@@ -96,6 +100,11 @@ const char* nccl_load(void)
 int nccl_unique_id(NcclUid* id) { return g_nccl.GetUniqueId(id); }
 int nccl_comm_init(void** comm, int nranks, const NcclUid* id, int rank) { return g_nccl.CommInitRank(comm, nranks, *id, rank); }
 void nccl_comm_destroy(void* comm) { if (comm && g_nccl.ok) g_nccl.CommDestroy(comm); }
+int nccl_comm_split(void* comm, int rank, void** out)
+{
+    if (!g_nccl.ok || !g_nccl.CommSplit) return -1;
+    return g_nccl.CommSplit(comm, 0, rank, out, nullptr);
+}
 const char* nccl_error_string(int rc) { return g_nccl.ok ? g_nccl.GetErrorString(rc) : "nccl not loaded"; }
 
 // ------------------------------------------------------------------------------------
@@ -416,10 +425,21 @@ static cudaError_t launch_fwd(Ctx* s, const SlabCf& C, const SlabArgs& a, int nc
     return cudaGetLastError();
 }
 
-// exchange layouts (ns slots per part, nb = Q + 2 values back per line and component):
-//   EMULATE  UP [master][rank][Q][ns][nidx], DN [rank][master][3][nb][nidx] (shared)
-//   NCCL     up_s [master][Q][ns][nidx] -> up_rv [rank][Q][ns][nidx] (all-to-all),
-//            dn_s [rank][3][nb][nidx]   -> dn_rv [master][3][nb][nidx]
+// exchange layouts (ns slots per part, nb = Q + 2 values back per line and component),
+// one set per rank -- with EMULATE, slab r's set sits at r * (per-rank size) in the
+// same buffers, so both transports run the same layouts and only the copy primitive
+// differs (ncclSend/ncclRecv pairs, or one device copy per (sender, receiver) block):
+//   up_s  [master][Q][ns][nidx]  -> up_rv [rank][Q][ns][nidx]   (scalars to the masters)
+//   dn_s  [rank][3][nb][nidx]    -> dn_rv [master][3][nb][nidx] (y values back)
+static size_t up_rank_size(const Group* G, long long plane)
+{
+    return (size_t)G->P * G->Q * kSlabSlots * (size_t)(plane / G->P);
+}
+static size_t dn_rank_size(const Group* G, long long plane)
+{
+    return (size_t)G->P * 3 * (size_t)(G->Q + 2) * (size_t)(plane / G->P);
+}
+
 static SlabArgs slab_args(Ctx* s, Group* G, int ns)
 {
     SlabArgs a{};
@@ -437,25 +457,17 @@ static SlabArgs slab_args(Ctx* s, Group* G, int ns)
     a.nidx = (int)(s->plane / P);
     a.nb = Q + 2;
     const long long NI = a.nidx, blk = (long long)Q * ns * NI, blk2 = 3LL * a.nb * NI;
-    if (G->transport == IB_TRANSPORT_EMULATE) {
-        a.up_w = G->up_s + (long long)s->rank * blk;
-        a.up_mstride = (long long)P * blk;
-        a.up_r = G->up_s;
-        a.up_rmstride = (long long)P * blk;
-        a.dn_w = G->dn_s;
-        a.dn_wmstride = blk2;
-        a.dn_rstride = (long long)P * blk2;
-        a.dn_r = G->dn_s + (long long)s->rank * P * blk2;
-    } else {
-        a.up_w = G->up_s;
-        a.up_mstride = blk;
-        a.up_r = G->up_rv;
-        a.up_rmstride = 0;
-        a.dn_w = G->dn_s;
-        a.dn_wmstride = 0;
-        a.dn_rstride = blk2;
-        a.dn_r = G->dn_rv;
-    }
+    const bool emu = G->transport == IB_TRANSPORT_EMULATE;
+    const long long us = (long long)up_rank_size(G, s->plane), ds = (long long)dn_rank_size(G, s->plane);
+    const long long me = emu ? s->rank : 0;               // this slab's buffer set
+    a.up_w = G->up_s + me * us;
+    a.up_mstride = blk;
+    a.up_r = G->up_rv;                                    // the master kernel's z-th master
+    a.up_rmstride = emu ? us : 0;
+    a.dn_w = G->dn_s;
+    a.dn_wmstride = emu ? ds : 0;
+    a.dn_rstride = blk2;
+    a.dn_r = G->dn_rv + me * ds;
     return a;
 }
 
@@ -659,15 +671,18 @@ __global__ void k_sum_slots(const double* __restrict__ part, int P, long long cn
 
 // Steps 1b-1c on every point from the reduced U^n (identical on every rank)
 __global__ void k_evolve(const double* __restrict__ U, double* __restrict__ X, double* __restrict__ Xh,
-                         double* __restrict__ Uprev, long long cnt, double dt, int first)
+                         double* __restrict__ Uprev, double* __restrict__ Xold, double* __restrict__ Uold,
+                         long long cnt, double dt, int first)
 {
     const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (e >= cnt) return;
-    const double x = X[e], u = U[e];
-    const double xn = first ? x + dt * u : x + dt * (1.5 * u - 0.5 * Uprev[e]);
+    const double x = X[e], u = U[e], up = Uprev[e];
+    const double xn = first ? x + dt * u : x + dt * (1.5 * u - 0.5 * up);
     Xh[e] = 0.5 * (xn + x);
     X[e] = xn;
     Uprev[e] = u;
+    Xold[e] = x;        // X^n, U^{n-1}: the state before this IB phase (read while ahead)
+    Uold[e] = up;
 }
 
 // Step 2b restricted to the nodes this slab owns (into G = N^{n-1} + (2/rho) f, R24)
@@ -744,12 +759,26 @@ static cudaError_t slab_select(Ctx* top, Ctx* s, const double* Xsrc, int* list, 
     return cudaGetLastError();
 }
 
+// the slab IB kernels: one thread per (point, component) for the interpolation and the
+// quad-lane spread with warp pre-reduction (ib.cu) on the selected points; IBGM_SLAB_IB=0
+// keeps the per-point kernels below (A/B)
+static bool slab_ib_fast()
+{
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("IBGM_SLAB_IB");
+        v = (e && atoi(e) == 0) ? 0 : 1;
+    }
+    return v == 1;
+}
+
 cudaError_t slab_interp_part(Ctx* top, Ctx* s, double* Upart, int* list, int* count)
 {
     const double invh = 1.0 / s->h;
     cudaError_t e = cudaMemsetAsync(Upart, 0, sizeof(double) * top->npts * top->dim, s->stream);
     if (e != cudaSuccess) return e;
     if ((e = slab_select(top, s, top->X, list, count)) != cudaSuccess) return e;
+    if (slab_ib_fast()) return launch_interp_part(top, s, Upart, list, count);
 #define IBGM_IP(D, K) k_interp_part<D, K><<<nb128(top->npts), 128, 0, s->stream>>>( \
         s->u[0], s->u[1], s->u[2], top->X, Upart, list, count, (int)s->n, (int)s->z0, (int)s->nl, invh)
     if (s->dim == 2) { if (top->kernel == IB_DELTA_COS4) IBGM_IP(2, 0); else IBGM_IP(2, 1); }
@@ -770,7 +799,8 @@ cudaError_t slab_sum_slots(Ctx* top, const double* part, int P, double* out)
 cudaError_t slab_evolve(Ctx* top, const double* U, int first)
 {
     const long long cnt = top->npts * top->dim;
-    k_evolve<<<nb128(cnt), 128, 0, top->stream>>>(U, top->X, top->Xh, top->Uprev, cnt, top->dt, first);
+    k_evolve<<<nb128(cnt), 128, 0, top->stream>>>(U, top->X, top->Xh, top->Uprev, top->Xold, top->Uold, cnt, top->dt,
+                                                  first);
     top->launches++;
     return cudaGetLastError();
 }
@@ -782,6 +812,7 @@ cudaError_t slab_spread_part(Ctx* top, Ctx* s, int* list, int* count)
     const bool kp = top->debug_keep_f != 0;
     cudaError_t e = slab_select(top, s, top->Xh, list, count);
     if (e != cudaSuccess) return e;
+    if (slab_ib_fast()) return launch_spread_part(top, s, list, count);
 #define IBGM_SPP(D, K, KP) k_spread_part<D, K, KP><<<nb128(top->npts), 128, 0, s->stream>>>(                  \
         top->Xh, top->F, top->wgt, s->nprev[0], s->nprev[1], s->nprev[2], s->f[0], s->f[1], s->f[2], list, count, \
         (int)s->n, (int)s->z0, (int)s->nl, invh, invhd, 2.0 / s->rho)
@@ -806,6 +837,45 @@ cudaError_t slab_spread_part(Ctx* top, Ctx* s, int* list, int* count)
         if (r_ != 0) return r_;                     \
     } while (0)
 
+// EMULATE transport: the P x P (sender, receiver) block copies of one all-to-all in a
+// single launch -- block (r, m) of `cnt` doubles goes from src + r sr + m sm to
+// dst + m dr + r dm (blockIdx.y = r P + m), exactly the ncclSend/ncclRecv pairs of the
+// NCCL transport.
+__global__ void k_alltoall_copy(const double* __restrict__ src, double* __restrict__ dst, int P, long long cnt,
+                                long long sr, long long sm, long long dr, long long dm)
+{
+    const int r = blockIdx.y / P, m = blockIdx.y - r * P;
+    const double* a = src + r * sr + m * sm;
+    double* b = dst + m * dr + r * dm;
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < cnt; q += (long long)gridDim.x * blockDim.x)
+        b[q] = a[q];
+}
+
+static cudaError_t alltoall_copy(const double* src, double* dst, int P, long long cnt, long long sr, long long sm,
+                                 long long dr, long long dm, cudaStream_t st)
+{
+    const long long bx = std::min((cnt + 255) / 256, 64LL);
+    k_alltoall_copy<<<dim3((unsigned)std::max(bx, 1LL), (unsigned)(P * P)), 256, 0, st>>>(src, dst, P, cnt, sr, sm, dr,
+                                                                                        dm);
+    return cudaGetLastError();
+}
+
+// Halo exchange (EMULATE): every slab's boundary planes of up to kHaloMax fields into the
+// neighbours' halo planes in one launch (blockIdx.y = field, slab, direction)
+constexpr int kHaloMax = 4;
+struct HaloPtrs {
+    const double* src[kHaloMax * kMaxRanks * 2];
+    double* dst[kHaloMax * kMaxRanks * 2];
+};
+__global__ void k_halo_copy(const HaloPtrs H, long long PL)
+{
+    const double* a = H.src[blockIdx.y];
+    double* b = H.dst[blockIdx.y];
+    if (!a) return;
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < PL; q += (long long)gridDim.x * blockDim.x)
+        b[q] = a[q];
+}
+
 // Halo exchange of the listed fields.  dir_up: plane nz-1 of slab s
 // -> plane -1 of slab s+1; dir_down: plane 0 of slab s -> plane nz of slab s-1 (periodic).
 // Returns 0, a cudaError_t (as int, transport EMULATE) or an ncclResult_t (NCCL).
@@ -813,25 +883,29 @@ int group_halo(Group* G, int nf, const HaloSpec* spec, cudaStream_t st)
 {
     const int P = G->P;
     if (G->transport == IB_TRANSPORT_EMULATE) {
+        // the same sends and receives as the NCCL branch below, one launch for all of them
+        HaloPtrs H{};
+        int np = 0;
+        const long long nz = G->slab[0]->nl, PL = G->slab[0]->plane;
+        if (nf > kHaloMax) return (int)cudaErrorInvalidValue;
         for (int f = 0; f < nf; ++f)
             for (int r = 0; r < P; ++r) {
                 Ctx* a = G->slab[r];
-                const size_t pb = (size_t)a->plane * sizeof(double);
-                const long long nz = a->nl, PL = a->plane;
                 if (spec[f].up) {
                     Ctx* b = G->slab[(r + 1) % P];
-                    cudaError_t e = cudaMemcpyAsync(spec[f].field(b) - PL, spec[f].field(a) + (nz - 1) * PL, pb,
-                                                    cudaMemcpyDeviceToDevice, st);
-                    if (e != cudaSuccess) return (int)e;
+                    H.src[np] = spec[f].field(a) + (nz - 1) * PL;
+                    H.dst[np++] = spec[f].field(b) - PL;
                 }
                 if (spec[f].down) {
                     Ctx* b = G->slab[(r + P - 1) % P];
-                    cudaError_t e = cudaMemcpyAsync(spec[f].field(b) + nz * PL, spec[f].field(a), pb,
-                                                    cudaMemcpyDeviceToDevice, st);
-                    if (e != cudaSuccess) return (int)e;
+                    H.src[np] = spec[f].field(a);
+                    H.dst[np++] = spec[f].field(b) + nz * PL;
                 }
             }
-        return 0;
+        if (np == 0) return 0;
+        const long long bx = std::min((PL + 255) / 256, 32LL);
+        k_halo_copy<<<dim3((unsigned)bx, (unsigned)np), 256, 0, st>>>(H, PL);
+        return (int)cudaGetLastError();
     }
     Ctx* a = G->slab[0];
     const long long nz = a->nl, PL = a->plane;
@@ -852,11 +926,16 @@ int group_halo(Group* G, int nf, const HaloSpec* spec, cudaStream_t st)
     return 0;
 }
 
-// each line's scalars to its master (all-to-all; EMULATE: the buffer is shared)
+// each line's scalars to its master (all-to-all): rank r's block for master m
+// (up_s[r] + m blk) lands in master m's receive buffer at r blk
 int group_up(Group* G, int ns, cudaStream_t st)
 {
-    if (G->transport == IB_TRANSPORT_EMULATE) return 0;
-    const size_t blk = (size_t)G->Q * ns * (G->slab[0]->plane / G->P);
+    const long long plane = G->slab[0]->plane;
+    const size_t blk = (size_t)G->Q * ns * (plane / G->P);
+    if (G->transport == IB_TRANSPORT_EMULATE) {
+        const long long us = (long long)up_rank_size(G, plane);
+        return (int)alltoall_copy(G->up_s, G->up_rv, G->P, (long long)blk, us, (long long)blk, us, (long long)blk, st);
+    }
     NCK(g_nccl.GroupStart());
     for (int m = 0; m < G->P; ++m) {
         NCK(g_nccl.Send(G->up_s + m * blk, blk, kNcclDouble, m, G->comm, st));
@@ -866,12 +945,19 @@ int group_up(Group* G, int ns, cudaStream_t st)
     return 0;
 }
 
-// the masters' y values and corrections back to the ranks (all-to-all)
+// the masters' y values and corrections back to the ranks (all-to-all): master m's
+// block for rank r (dn_s[m] + r stride) lands in rank r's receive buffer at m stride
 int group_dn(Group* G, int ncomp, cudaStream_t st)
 {
-    if (G->transport == IB_TRANSPORT_EMULATE) return 0;
-    const size_t NI = G->slab[0]->plane / G->P, nb = (size_t)G->Q + 2;
+    const long long plane = G->slab[0]->plane;
+    const size_t NI = plane / G->P, nb = (size_t)G->Q + 2;
     const size_t stride = 3 * nb * NI, cnt = (size_t)ncomp * nb * NI;
+    if (G->transport == IB_TRANSPORT_EMULATE) {
+        // sender = master m (block for rank r at r stride) -> receiver r (at m stride)
+        const long long ds = (long long)dn_rank_size(G, plane);
+        return (int)alltoall_copy(G->dn_s, G->dn_rv, G->P, (long long)cnt, ds, (long long)stride, ds,
+                                  (long long)stride, st);
+    }
     NCK(g_nccl.GroupStart());
     for (int r = 0; r < G->P; ++r) {
         NCK(g_nccl.Send(G->dn_s + r * stride, cnt, kNcclDouble, r, G->comm, st));
@@ -882,11 +968,11 @@ int group_dn(Group* G, int ncomp, cudaStream_t st)
 }
 
 // U^n = sum over ranks of the partial interpolations
-int group_allreduce_U(Group* G, Ctx* top, cudaStream_t st)
+int group_allreduce_U(Group* G, Ctx* top, cudaStream_t st, bool side)
 {
     const long long cnt = top->npts * top->dim;
     if (G->transport == IB_TRANSPORT_EMULATE) return (int)slab_sum_slots(top, G->Upart, G->P, G->Ured);
-    return g_nccl.AllReduce(G->Upart, G->Ured, (size_t)cnt, kNcclDouble, kNcclSum, G->comm, st);
+    return g_nccl.AllReduce(G->Upart, G->Ured, (size_t)cnt, kNcclDouble, kNcclSum, side ? G->comm_side : G->comm, st);
 }
 
 }  // namespace ibgm
