@@ -26,6 +26,10 @@ def phase_of(name, grid):
         return "force"
     if name.startswith("k_spread") or name.startswith("k_brick"):
         return "spread"
+    if name.startswith("k_xwarp"):
+        # k_xwarp<L, KIND, DIM, NC, WPB, MINB>: x-line passes
+        args = [a.strip() for a in name[name.index("<") + 1:name.index(">")].split(",")]
+        return "s1_rhs_xsweep" if int(args[1]) == 0 else "psi_x_p"
     if name.startswith("k_lines") or name.startswith("k_strided"):
         # k_lines<L, KIND, DIM, AX, ...>, k_strided<L, KIND, DIM, AX>
         args = [a.strip() for a in name[name.index("<") + 1:name.index(">")].split(",")]
@@ -84,9 +88,10 @@ with open(os.path.join(out_dir, f"{tag}_ncu_full.txt"), "w") as f:
         us = g("gpu__time_duration.sum")
         rd, wr = g("dram__bytes_read.sum"), g("dram__bytes_write.sum")
         units = r[1]
-        scale = 1e6 if units[jx["dram__bytes_read.sum"]].lower().startswith("mbyte") else (
-            1e3 if units[jx["dram__bytes_read.sum"]].lower().startswith("kbyte") else 1.0)
+        u = units[jx["dram__bytes_read.sum"]].lower()
+        scale = {"gbyte": 1e9, "mbyte": 1e6, "kbyte": 1e3}.get(u, 1.0)   # -> bytes
         traffic.setdefault(ph, (rd + wr) * scale)
+        rd, wr = rd * scale / 1e6, wr * scale / 1e6                        # MB in the table
         f.write(f"{ph:16s} | {us:7.1f} | {rd:8.1f} | {wr:8.1f} | {g(M[3]):5.1f} | {g(M[4]):5.1f} | {g(M[5]):5.1f} | "
                 f"{g(M[6]):5.1f} | {g(M[7]):5.1f} | {g(M[8]):4.0f} | {grid}  {nm}\n")
 json.dump(traffic, open(os.path.join(out_dir, f"traffic_cfg{cfg}.json"), "w"), indent=1)
