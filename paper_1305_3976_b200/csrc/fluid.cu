@@ -253,8 +253,14 @@ __device__ __forceinline__ RowB row_bases(int j, int k, int n, int nl, int wrap)
 //   N_c = 1/(4h) sum_j [ (u_j(I+e_j) + u_j(I+e_j-e_c)) u_c(I+e_j) - (u_j(I) + u_j(I-e_c)) u_c(I-e_j) ]
 // L2 prefetch of the operands that miss in L1/L2 for cell i of a row (its centre, its
 // z-neighbour planes, the history G and p*), issued one row ahead by the fill loop
+// k_xwarp S1: warps per block and blocks per SM the registers must allow (measured at
+// config 4, graph ms/step: 4 warps x 4 blocks 4.90-4.95, 8 x 2 4.86-4.89, 16 x 1 4.92-4.97,
+// 2 x 8 5.22, 6 x 2 5.08)
 #ifndef IBGM_S1_MINB
-#define IBGM_S1_MINB 4
+#define IBGM_S1_MINB 2
+#endif
+#ifndef IBGM_XWARP_WPB
+#define IBGM_XWARP_WPB 8
 #endif
 #ifndef IBGM_S1_PREFETCH
 #define IBGM_S1_PREFETCH 1
@@ -931,7 +937,7 @@ static cudaError_t go_lines(Ctx* s, int sys, const LArgs& a, int ncomp_grid)
         // measured (graph ms/step): config 4 (384^3) 5.056 -> 4.957; config 3 (128^3) 0.1686 ->
         // 0.1724 and config 2 (1024^2) 0.066 -> 0.075 slower, so only 3D grids of N >= 256
         if (xwarp_enabled() && DIM == 3 && s->n >= 256 && s->P <= 32) {
-            constexpr int WPB = 4;
+            constexpr int WPB = (KIND == K_S1) ? IBGM_XWARP_WPB : 4;
             constexpr int MINB = (KIND == K_S1) ? IBGM_S1_MINB : 8;
             auto kern = k_xwarp<L, KIND, DIM, NC, WPB, MINB>;
             const int lpw = 32 / s->P;
