@@ -615,10 +615,15 @@ int ib_create(const ib_grid* grid, double nu, double rho, double dt, const ib_op
         // that their blocks take SM slots as the psi passes' blocks retire
         int prio_lo = 0, prio_hi = 0;
         CKC(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
-        CKC(cudaStreamCreateWithPriority(&s->side, cudaStreamNonBlocking, prio_hi));
+        // (A/B switches: IBGM_LOOKAHEAD=0 runs the IB phase in line; IBGM_SIDE_PRIO=0 gives
+        //  the side stream the default priority)
+        const char* ep = getenv("IBGM_SIDE_PRIO");
+        const int prio = (ep && atoi(ep) == 0) ? prio_lo : prio_hi;
+        CKC(cudaStreamCreateWithPriority(&s->side, cudaStreamNonBlocking, prio));
         CKC(cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming));
         CKC(cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming));
-        s->lookahead = 1;
+        const char* el = getenv("IBGM_LOOKAHEAD");
+        s->lookahead = (el && atoi(el) == 0) ? 0 : 1;
     }
     // brick grid for the binned spread: 4^3 cells (3D) / 8^2 (2D)
     {

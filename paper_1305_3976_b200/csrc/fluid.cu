@@ -446,7 +446,7 @@ struct LinePass {
         const unsigned RTP = (unsigned)R * TP;
         const int nrow = (DIM == 2) ? A.nl : n;
         if (KIND == K_S1) {
-            if (n >= T && A.s1flat) {
+            if (n >= T && A.s1flat == 1) {
                 // the tile's R x n cells flattened over the threads (n = 384 on 256 threads:
                 // 12 cells each instead of two rounds per row with half the threads idle)
                 const int lmax = min(R, nrow - g0);
@@ -466,13 +466,15 @@ struct LinePass {
                     for (int c = 0; c < NC; ++c) tile[c * RTP + off] = v[c];
                 }
             } else if (n >= T) {
-                    for (int l = 0; l < R && g0 + l < nrow; ++l) {
+                for (int l = 0; l < R && g0 + l < nrow; ++l) {
                     const RowB rb = row_bases<DIM>(g0 + l, (int)tb, n, A.nl, A.wrap);
                     if (l + IBGM_PF_ROWS < R && g0 + l + IBGM_PF_ROWS < nrow) {
                         const RowB rn = row_bases<DIM>(g0 + l + IBGM_PF_ROWS, (int)tb, n, A.nl, A.wrap);
                         for (int m = t; m < n; m += T) s1_prefetch<DIM>(A.s1, m, rn);
                     }
                     for (int m = t; m < n; m += T) {
+                        // (a warp-owned row, A.s1flat == 2: prefetch this row two steps ahead)
+                        if (A.s1flat == 2 && m + IBGM_PF_DIST * T < n) s1_prefetch<DIM>(A.s1, m + IBGM_PF_DIST * T, rb);
                         double v[3];
                         s1_cell<DIM>(A.s1, m, rb, n, v);
                         const int off = tile_off<L>(l, m, TP);
@@ -947,7 +949,15 @@ static cudaError_t go_lines(Ctx* s, int sys, const LArgs& a, int ncomp_grid)
             static unsigned long long attr_mask = 0;
             const cudaError_t ae = smem_attr_once(attr_mask, kern, (int)smem_limit());
             if (ae != cudaSuccess) return ae;
-            la.s1flat = 1;
+            {
+                // IBGM_XFLAT=1: the flattened fill (row and cell from one index per cell)
+                static int fl = -1;
+                if (fl < 0) {
+                    const char* e = getenv("IBGM_XFLAT");
+                    fl = (e && atoi(e) == 1) ? 1 : 2;
+                }
+                la.s1flat = fl;
+            }
             const dim3 grid((unsigned)((rows + WPB * lpw - 1) / (WPB * lpw)), (unsigned)gy, 1u);
             kern<<<grid, 32 * WPB, sm, s->stream>>>(s->hcoef[sys], s->sinv + sys, (int)s->n, la);
             s->launches++;
