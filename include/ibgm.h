@@ -240,7 +240,7 @@ int ib_get_stats(ib_ctx* ctx, double* ms_per_phase, int64_t* steps_done, int64_t
 
 /* Debug flags: bit 0 keeps the spread force f^{n+1/2} as a separate field so that
  * ib_get_aux can return it (costs one extra atomic per spread contribution and a
- * clear per step).  Bits 1-3 select the spreading method: 0 automatic (5 in 3D,
+ * clear per step).  Bits 1-3 select the spreading method: 0 automatic (6 in 3D,
  * 4 in 2D),
  * 1 one thread per point (4^d global fp64 reductions per component), 2 brick-binned
  * (points counting-sorted into 4^3-cell bricks every step, shared-memory tiles),
@@ -248,14 +248,18 @@ int ib_get_stats(ib_ctx* ctx, double* ms_per_phase, int64_t* steps_done, int64_t
  * one global reduction per box node), 4 quad-lane (4 lanes per point and component,
  * one per x-node of a stencil row, so each warp reduction is coalesced), 5 quad-lane
  * with a warp pre-reduction (consecutive points of a warp with the same base node sum
- * their contributions by shuffles and one lane group issues the reductions).  Bits 4-6
- * select the interpolation: 0 automatic (3 in 2D, 4 in 3D), 1 one thread per point, 2 box-staged,
- * 3 quad-lane, 4 one thread per (point, component).  The points are kept internally in Morton order of their initial
+ * their contributions by shuffles and one lane group issues the reductions), 6 window-
+ * staged (a warp accumulates the contributions of 32 consecutive points into a
+ * shared-memory box of their supports without atomics, then one global reduction per
+ * non-zero box node).  Bits 4-6
+ * select the interpolation: 0 automatic (3 in 2D, 5 in 3D), 1 one thread per point, 2 box-staged,
+ * 3 quad-lane, 4 one thread per (point, component), 5 window-staged (a warp loads the
+ * box of u covering the supports of 32 consecutive points into shared memory once).  The points are kept internally in Morton order of their initial
  * cells (outputs are returned in the caller's order).  Automatic by default.  Only
  * the single-GPU path honours bits 1-6.  Set bit 0 before the first ib_step (or right
  * after ib_set_fields): once the look-ahead has run the next step's IB phase, turning
- * it on returns IB_ESTATE.  Errors: IB_EINVAL (spreading method > 5, interpolation
- * method > 4, or a bit above 6 set). */
+ * it on returns IB_ESTATE.  Errors: IB_EINVAL (spreading method > 6, interpolation
+ * method > 5, or a bit above 6 set). */
 int ib_set_debug(ib_ctx* ctx, int32_t flags);
 
 /* Turn per-phase CUDA-event timing on (1) or off (0).  While on, ib_step records an

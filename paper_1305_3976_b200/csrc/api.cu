@@ -1139,8 +1139,8 @@ int ib_set_debug(ib_ctx* c, int32_t flags)
 {
     if (!c) return fail(IB_EINVAL, "null context");
     Ctx* s = &c->s;
-    if (((flags >> 1) & 7) > 5 || ((flags >> 4) & 7) > 4 || (flags >> 7) != 0)
-        return fail(IB_EINVAL, "debug flags 0x%x: spreading method > 5, interpolation method > 4 or unknown bits",
+    if (((flags >> 1) & 7) > 6 || ((flags >> 4) & 7) > 5 || (flags >> 7) != 0)
+        return fail(IB_EINVAL, "debug flags 0x%x: spreading method > 6, interpolation method > 5 or unknown bits",
                     (unsigned)flags);
     const int keep = (flags & 1) != 0;
     if (keep && !s->debug_keep_f && s->ib_ahead)

@@ -1021,6 +1021,340 @@ __global__ void __launch_bounds__(256) k_spread_quad(const double* __restrict__ 
     }
 }
 
+// -------------------------------------------------------------------------------
+// Window-staged spreading and interpolation (Steps 2b and 1a).  A warp takes a window
+// of 32 consecutive points (Morton order, R30) and one velocity component in 3D (both
+// components, one per half-warp, in 2D).  The 4^d supports of a window's points overlap
+// heavily (dense membranes: at config 4 a window of 32 points touches ~170 distinct
+// nodes, against 32 x 64 contributions), so the warp works in a box of shared memory
+// covering the window's supports (origin = the smallest base node, extents = spread of
+// the base nodes + 4):
+//   spreading      iterates over the window's points; for each point the lanes own the
+//                  distinct nodes of its support (2 per lane in 3D, 1 per half-warp lane
+//                  in 2D) and add their contributions to the box -- no two lanes touch
+//                  the same entry in one iteration, so no atomics -- then every non-zero
+//                  box entry goes to G (and f) with ONE global fp64 reduction;
+//   interpolation  loads the box of u_c once (rows contiguous along x) and every lane
+//                  gathers its point's 4^d stencil from shared memory.
+// Only warp barriers: warps never wait for each other.  A window whose box exceeds the
+// budget (points far apart, or a window across the periodic seam) falls back to direct
+// global reductions / gathers, so results never depend on the ordering.
+// -------------------------------------------------------------------------------
+template <int DIM>
+struct WinCfg {
+    static constexpr int CPW = (DIM == 3) ? 1 : 2;             // components per warp
+    static constexpr int WPW = DIM / CPW;                      // warps per window
+    static constexpr int CAP = (DIM == 3) ? 640 : 320;         // box doubles per component
+    static constexpr int REC = 4 * DIM;                        // per point: w_x F, w_y[, w_z]
+    static constexpr int WARP_DOUBLES = CPW * (CAP + 32 * REC);
+    static constexpr int WARP_INTS = CPW * 32;
+};
+
+template <int DIM>
+__host__ __device__ constexpr size_t win_smem(int warps)
+{
+    return (size_t)warps * (WinCfg<DIM>::WARP_DOUBLES * sizeof(double) + WinCfg<DIM>::WARP_INTS * sizeof(int));
+}
+
+// box entry i -> unwrapped offsets (x, y, z) inside a box of extents e (exact for the
+// box sizes used: i < 2^20)
+template <int DIM>
+__device__ __forceinline__ void win_unflat(int i, const int e[3], float r0, float r01, int& x, int& y, int& z)
+{
+    if (DIM == 3) {
+        z = (int)((float)i * r01 + 0.5f * r01);
+        const int rem = i - z * e[0] * e[1];
+        y = (int)((float)rem * r0 + 0.5f * r0);
+        x = rem - y * e[0];
+    } else {
+        z = 0;
+        y = (int)((float)i * r0 + 0.5f * r0);
+        x = i - y * e[0];
+    }
+}
+
+// window bounding box of the lanes' base nodes (unwrapped); false if it does not fit
+template <int DIM, int CAP>
+__device__ __forceinline__ bool win_box(const int bl[3], bool valid, int n, int o[3], int e[3], int& V)
+{
+    const unsigned FULL = 0xffffffffu;
+    bool ok = true;
+    V = 1;
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) {
+        const int lo = __reduce_min_sync(FULL, valid ? bl[a] : INT_MAX);
+        const int hi = __reduce_max_sync(FULL, valid ? bl[a] : INT_MIN);
+        o[a] = lo;
+        e[a] = (hi >= lo) ? hi - lo + 4 : 1;
+        ok = ok && e[a] <= CAP && e[a] <= n;
+    }
+    if (!ok) return false;
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) V *= e[a];
+    return V <= CAP;
+}
+
+template <int DIM, int KER, bool KEEP, bool PART>
+__global__ void __launch_bounds__(256) k_spread_win(const double* __restrict__ Xh, const double* __restrict__ F,
+                                                    const double* __restrict__ wgt, double* __restrict__ g0,
+                                                    double* __restrict__ g1, double* __restrict__ g2,
+                                                    double* __restrict__ f0, double* __restrict__ f1,
+                                                    double* __restrict__ f2, int64_t npts, int n, double invh,
+                                                    double invhd, double two_rho, const int* __restrict__ list,
+                                                    const int* __restrict__ count, int z0, int nzl)
+{
+    using W = WinCfg<DIM>;
+    constexpr int CPW = W::CPW, CAP = W::CAP, REC = W::REC;
+    extern __shared__ double wsm[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    double* box = wsm + (size_t)wib * W::WARP_DOUBLES;          // [CPW][CAP]
+    double* rec = box + CPW * CAP;                              // [CPW][32][REC]
+    int* rel = (int*)(wsm + (size_t)(blockDim.x >> 5) * W::WARP_DOUBLES) + wib * W::WARP_INTS;   // [CPW][32]
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t win = gw / W::WPW;
+    const int cw = (int)(gw - win * W::WPW);
+    const int64_t nitem = PART ? (int64_t)*count : npts;
+    if (win * 32 >= nitem) return;                              // warp-uniform
+    const int64_t item = win * 32 + lane;
+    const bool valid = item < nitem;
+    int64_t k = valid ? item : 0;
+    if (PART && valid) k = list[item];
+    double Xk[3] = {0, 0, 0};
+    double ws = 0.0;
+    if (valid) {
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) Xk[a] = Xh[k * DIM + a];
+        ws = wgt[k] * invhd;
+    }
+    const int nv = __popc(__ballot_sync(0xffffffffu, valid));  // valid lanes are a prefix
+    const size_t nn = (size_t)n;
+    int bl[CPW][3], o[CPW][3], e[CPW][3], V[CPW];
+    double w[CPW][3][4];
+    bool fits[CPW];
+#pragma unroll
+    for (int q = 0; q < CPW; ++q) {
+        const int c = (DIM == 3) ? cw : q;
+        bl[q][2] = 0;
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) weights4u<KER>(Xk[a] * invh - (a == c ? 0.0 : 0.5), bl[q][a], w[q][a]);
+        const double Fs = valid ? F[k * DIM + c] * ws : 0.0;
+#pragma unroll
+        for (int m = 0; m < 4; ++m) w[q][0][m] *= Fs;
+        fits[q] = win_box<DIM, CAP>(bl[q], valid, n, o[q], e[q], V[q]);
+        if (fits[q]) {
+            double* R = rec + (q * 32 + lane) * REC;
+#pragma unroll
+            for (int a = 0; a < DIM; ++a)
+#pragma unroll
+                for (int m = 0; m < 4; ++m) R[4 * a + m] = w[q][a][m];
+            rel[q * 32 + lane] = (bl[q][0] - o[q][0]) + e[q][0] * ((bl[q][1] - o[q][1]) +
+                                                                 (DIM == 3 ? e[q][1] * (bl[q][2] - o[q][2]) : 0));
+            for (int i = lane; i < V[q]; i += 32) box[q * CAP + i] = 0.0;
+        }
+    }
+    __syncwarp();
+    // accumulate: point by point, the lanes own distinct nodes of its support
+    if (DIM == 3) {
+        if (fits[0]) {
+            const int dx = lane & 3, dy = (lane >> 2) & 3, dz = lane >> 4;
+            const int e01 = e[0][0] * e[0][1];
+            const int loff = dx + e[0][0] * dy + e01 * dz;
+            const int st2 = 2 * e01;
+            for (int p = 0; p < nv; ++p) {
+                const double* R = rec + p * REC;
+                const int r = rel[p] + loff;
+                const double a = R[dx] * R[4 + dy];
+                const double v0 = a * R[8 + dz], v1 = a * R[10 + dz];
+                box[r] += v0;
+                box[r + st2] += v1;
+                __syncwarp();
+            }
+        }
+    } else {
+        const int h = lane >> 4, j = lane & 15;
+        const int dx = j & 3, dy = j >> 2;
+        const bool fh = h ? fits[CPW - 1] : fits[0];
+        const int eh = h ? e[CPW - 1][0] : e[0][0];
+        const int loff = dx + eh * dy;
+        double* bh = box + h * CAP;
+        const double* rh = rec + h * 32 * REC;
+        const int* relh = rel + h * 32;
+        for (int p = 0; p < nv; ++p) {
+            if (fh) {
+                const double* R = rh + p * REC;
+                bh[relh[p] + loff] += R[dx] * R[4 + dy];
+            }
+            __syncwarp();
+        }
+    }
+    // flush: one reduction per non-zero box entry; fall back to direct reductions
+#pragma unroll
+    for (int q = 0; q < CPW; ++q) {
+        const int c = (DIM == 3) ? cw : q;
+        double* gc = (c == 0) ? g0 : (c == 1 ? g1 : g2);
+        double* fc = (c == 0) ? f0 : (c == 1 ? f1 : f2);
+        if (fits[q]) {
+            int wo[3] = {0, 0, 0};
+#pragma unroll
+            for (int a = 0; a < DIM; ++a) wo[a] = wrapm(o[q][a], n);
+            const float r0 = 1.0f / (float)e[q][0];
+            const float r01 = 1.0f / (float)(e[q][0] * e[q][1]);
+            for (int i = lane; i < V[q]; i += 32) {
+                const double v = box[q * CAP + i];
+                if (v == 0.0) continue;
+                int x, y, z;
+                win_unflat<DIM>(i, e[q], r0, r01, x, y, z);
+                int gx = wo[0] + x, gy = wo[1] + y, gz = wo[2] + z;
+                if (gx >= n) gx -= n;
+                if (gy >= n) gy -= n;
+                if (gz >= n) gz -= n;
+                int ll = (DIM == 3) ? gz : gy;                  // the last axis
+                if (PART) {
+                    ll -= z0;
+                    if ((unsigned)ll >= (unsigned)nzl) continue;
+                }
+                const size_t qa = (DIM == 3) ? nn * (nn * (size_t)ll + gy) + gx : nn * (size_t)ll + gx;
+                atomicAdd(gc + qa, two_rho * v);
+                if (KEEP) atomicAdd(fc + qa, v);
+            }
+        } else if (valid) {
+            int wb[3] = {0, 0, 0};
+#pragma unroll
+            for (int a = 0; a < DIM; ++a) wb[a] = wrapm(bl[q][a], n);
+            const int m2n = (DIM == 3) ? 4 : 1;
+            for (int m2 = 0; m2 < m2n; ++m2) {
+                const int gz = (DIM == 3) ? wrap1(wb[2] + m2, n) : 0;
+#pragma unroll
+                for (int m1 = 0; m1 < 4; ++m1) {
+                    const int gy = wrap1(wb[1] + m1, n);
+                    int ll = (DIM == 3) ? gz : gy;
+                    if (PART) {
+                        ll -= z0;
+                        if ((unsigned)ll >= (unsigned)nzl) continue;
+                    }
+                    const double a1 = w[q][1][m1] * ((DIM == 3) ? w[q][2][m2] : 1.0);
+#pragma unroll
+                    for (int m0 = 0; m0 < 4; ++m0) {
+                        const int gx = wrap1(wb[0] + m0, n);
+                        const size_t qa = (DIM == 3) ? nn * (nn * (size_t)ll + gy) + gx : nn * (size_t)ll + gx;
+                        const double v = a1 * w[q][0][m0];
+                        atomicAdd(gc + qa, two_rho * v);
+                        if (KEEP) atomicAdd(fc + qa, v);
+                    }
+                }
+            }
+        }
+    }
+}
+
+// Window-staged interpolation + Steps 1b-1c.  3D: a 192-thread block = 2 windows x 3
+// components (warp = window x component); the block barrier orders every read of X^n
+// before the writes of X^{n+1} (all components of a point are in the block).  2D: a warp
+// = one window, both components (boxes [2][CAP]), each lane owns one point.
+template <int DIM, int KER>
+__global__ void __launch_bounds__(256) k_interp_win(const double* __restrict__ u0, const double* __restrict__ u1,
+                                                    const double* __restrict__ u2, double* __restrict__ X,
+                                                    double* __restrict__ Xh, double* __restrict__ Uprev,
+                                                    double* __restrict__ Xold, double* __restrict__ Uold,
+                                                    int64_t npts, int n, double invh, double dt, int first)
+{
+    using W = WinCfg<DIM>;
+    constexpr int CPW = W::CPW, CAP = W::CAP;
+    extern __shared__ double wsm[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    double* box = wsm + (size_t)wib * CPW * CAP;
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t win = gw / W::WPW;
+    const int cw = (int)(gw - win * W::WPW);
+    const int64_t k = win * 32 + lane;
+    const bool valid = k < npts;
+    double Xk[3] = {0, 0, 0};
+    if (valid)
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) Xk[a] = X[k * DIM + a];
+    if (DIM == 3) __syncthreads();     // every X^n read of the block precedes any X^{n+1} write
+    if (win * 32 >= npts) return;      // warp-uniform
+    const size_t nn = (size_t)n;
+#pragma unroll
+    for (int q = 0; q < CPW; ++q) {
+        const int c = (DIM == 3) ? cw : q;
+        const double* uc = (c == 0) ? u0 : (c == 1 ? u1 : u2);
+        int bl[3] = {0, 0, 0}, o[3], e[3], V;
+        double w[3][4];
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) weights4u<KER>(Xk[a] * invh - (a == c ? 0.0 : 0.5), bl[a], w[a]);
+        const bool fits = win_box<DIM, CAP>(bl, valid, n, o, e, V);
+        double acc = 0.0;
+        if (fits) {
+            double* bq = box + q * CAP;
+            int wo[3] = {0, 0, 0};
+#pragma unroll
+            for (int a = 0; a < DIM; ++a) wo[a] = wrapm(o[a], n);
+            const float r0 = 1.0f / (float)e[0];
+            const float r01 = 1.0f / (float)(e[0] * e[1]);
+            for (int i = lane; i < V; i += 32) {
+                int x, y, z;
+                win_unflat<DIM>(i, e, r0, r01, x, y, z);
+                int gx = wo[0] + x, gy = wo[1] + y, gz = wo[2] + z;
+                if (gx >= n) gx -= n;
+                if (gy >= n) gy -= n;
+                if (gz >= n) gz -= n;
+                bq[i] = __ldg(uc + ((DIM == 3) ? nn * (nn * (size_t)gz + gy) + gx : nn * (size_t)gy + gx));
+            }
+            __syncwarp();
+            if (valid) {
+                const int rx = bl[0] - o[0], ry = bl[1] - o[1], rz = (DIM == 3) ? bl[2] - o[2] : 0;
+                const double* b0 = bq + rx + e[0] * (ry + e[1] * rz);
+                const int m2n = (DIM == 3) ? 4 : 1;
+#pragma unroll
+                for (int m2 = 0; m2 < m2n; ++m2) {
+                    double pa = 0.0;
+#pragma unroll
+                    for (int m1 = 0; m1 < 4; ++m1) {
+                        const double* row = b0 + e[0] * (m1 + e[1] * m2);
+                        double r = 0.0;
+#pragma unroll
+                        for (int m0 = 0; m0 < 4; ++m0) r += w[0][m0] * row[m0];
+                        pa += w[1][m1] * r;
+                    }
+                    acc += (DIM == 3) ? w[2][m2] * pa : pa;
+                }
+            }
+            __syncwarp();
+        } else if (valid) {
+            int wb[3] = {0, 0, 0};
+#pragma unroll
+            for (int a = 0; a < DIM; ++a) wb[a] = wrapm(bl[a], n);
+            const int m2n = (DIM == 3) ? 4 : 1;
+#pragma unroll
+            for (int m2 = 0; m2 < m2n; ++m2) {
+                const size_t pl = (DIM == 3) ? nn * nn * (size_t)wrap1(wb[2] + m2, n) : 0;
+                double pa = 0.0;
+#pragma unroll
+                for (int m1 = 0; m1 < 4; ++m1) {
+                    const size_t row = pl + nn * (size_t)wrap1(wb[1] + m1, n);
+                    double r = 0.0;
+#pragma unroll
+                    for (int m0 = 0; m0 < 4; ++m0) r += w[0][m0] * __ldg(uc + row + wrap1(wb[0] + m0, n));
+                    pa += w[1][m1] * r;
+                }
+                acc += (DIM == 3) ? w[2][m2] * pa : pa;
+            }
+        }
+        if (valid) {
+            // Steps 1b-1c for component c of this point
+            const double xc = (c == 0) ? Xk[0] : (c == 1 ? Xk[1] : Xk[2]);
+            const double up = Uprev[k * DIM + c];
+            const double xn = first ? xc + dt * acc : xc + dt * (1.5 * acc - 0.5 * up);
+            Xh[k * DIM + c] = 0.5 * (xn + xc);
+            X[k * DIM + c] = xn;
+            Uprev[k * DIM + c] = acc;
+            Xold[k * DIM + c] = xc;
+            Uold[k * DIM + c] = up;
+        }
+    }
+}
+
 // Step 1a restricted to the nodes of one z-slab (slab.cu): one thread per (listed point,
 // component), 64 points per 64*DIM block; the partial sums over ranks form U^n.
 template <int DIM, int KER>
@@ -1084,8 +1418,12 @@ cudaError_t launch_interp_part(Ctx* top, Ctx* s, double* Upart, const int* list,
     return cudaGetLastError();
 }
 
+template <bool PART>
+static cudaError_t launch_spread_win(Ctx* top, Ctx* s, const int* list, const int* count);
+
 cudaError_t launch_spread_part(Ctx* top, Ctx* s, const int* list, const int* count)
 {
+    if (s->dim == 3) return launch_spread_win<true>(top, s, list, count);
     const int64_t thr = ((top->npts + 7) / 8) * 8 * s->dim * 4;
     const unsigned nbk = (unsigned)((thr + 255) / 256);
     const double invh = 1.0 / s->h;
@@ -1154,10 +1492,32 @@ static cudaError_t box_attr(K kern, size_t sm)
 cudaError_t launch_interp_evolve(Ctx* s, int first)
 {
     if (s->npts == 0) return cudaSuccess;
-    // auto: quad-lane in 2D (config 2 0.0762 -> 0.0748 ms/step), per (point, component)
-    // in 3D (config 3 interp 20.4 -> 19.5 us, config 4 172 -> 162 us; quad-lane there:
-    // 0.1954 -> 0.2009 ms/step)
-    const int im = s->interp_mode ? s->interp_mode : (s->dim == 2 ? 3 : 4);
+    // auto: quad-lane in 2D (config 2 0.0762 -> 0.0748 ms/step; window-staged 0.0700),
+    // window-staged in 3D (config 4 interp 169 -> 140 us, 4.730 -> 4.710 ms/step; config 3
+    // 19.5 -> 17.7 us, 0.1695 -> 0.1680 ms/step, against one thread per (point, component))
+    const int im = s->interp_mode ? s->interp_mode : (s->dim == 2 ? 3 : 5);
+    if (im == 5) {
+        // window-staged: 3D 6 warps (2 windows x 3 components), 2D 8 warps (8 windows)
+        const int D = s->dim;
+        const int wpb = (D == 3) ? 6 : 8;
+        const int64_t warps = ((s->npts + 31) / 32) * (D == 3 ? 3 : 1);
+        const unsigned nbk = (unsigned)((warps + wpb - 1) / wpb);
+        const size_t sm = (size_t)wpb * (D == 3 ? WinCfg<3>::CPW * WinCfg<3>::CAP : WinCfg<2>::CPW * WinCfg<2>::CAP) *
+                          sizeof(double);
+        const double invh = 1.0 / s->h;
+#define IBGM_IW(Dd, K)                                                                                           \
+    do {                                                                                                         \
+        const cudaError_t ae_ = box_attr<300 + 10 * Dd + K>(k_interp_win<Dd, K>, sm);                           \
+        if (ae_ != cudaSuccess) return ae_;                                                                      \
+        k_interp_win<Dd, K><<<nbk, 32 * wpb, sm, s->stream>>>(s->u[0], s->u[1], s->u[2], s->X, s->Xh, s->Uprev, \
+                                                             s->Xold, s->Uold, s->npts, (int)s->n, invh, s->dt, first); \
+    } while (0)
+        if (D == 2) { if (s->kernel == IB_DELTA_COS4) IBGM_IW(2, 0); else IBGM_IW(2, 1); }
+        else { if (s->kernel == IB_DELTA_COS4) IBGM_IW(3, 0); else IBGM_IW(3, 1); }
+#undef IBGM_IW
+        s->launches++;
+        return cudaGetLastError();
+    }
     if (im == 3) {
         // a block holds whole 8-point groups of every component (32 DIM threads each):
         // 256 threads in 2D, 192 in 3D, so the X^n reads of all components of a point
@@ -1324,9 +1684,9 @@ static cudaError_t launch_spread_quad(Ctx* s)
     const double invh = 1.0 / s->h;
     const double invhd = (s->dim == 3) ? invh * invh * invh : invh * invh;
     const double two_rho = 2.0 / s->rho;
-    // auto: with the warp pre-reduction in 3D (config 4 spread 460 -> 348 us, config 3
-    // 30.3 -> 24.9 us), without in 2D (no runs of equal base nodes on a curve: no gain)
-    const int red = (s->spread_mode == 5 || (s->spread_mode == 0 && s->dim == 3)) ? 1 : 0;
+    // mode 5: with the warp pre-reduction (config 4 spread 460 -> 348 us, config 3
+    // 30.3 -> 24.9 us); 2D auto: without (no runs of equal base nodes on a curve)
+    const int red = (s->spread_mode == 5) ? 1 : 0;
 #define IBGM_SQ(D, K, KP) launch_pdl_if(D == 2, k_spread_quad<D, K, KP, false>, dim3(nbk), dim3(256), 0, s->stream, s->Xh, \
         s->F, s->wgt, s->nprev[0], s->nprev[1], s->nprev[2], s->f[0], s->f[1], s->f[2], s->npts, (int)s->n, invh, invhd, \
         two_rho, red, (const int*)nullptr, (const int*)nullptr, 0, 0)
@@ -1343,11 +1703,49 @@ static cudaError_t launch_spread_quad(Ctx* s)
     return cudaGetLastError();
 }
 
+// window-staged spreading (k_spread_win): 8 warps per block; PART: the listed points of
+// a z-slab (top: the replicated Lagrangian data, s: the slab)
+template <bool PART>
+static cudaError_t launch_spread_win(Ctx* top, Ctx* s, const int* list, const int* count)
+{
+    const int D = s->dim;
+    const int64_t warps = ((top->npts + 31) / 32) * (D == 3 ? 3 : 1);
+    const unsigned nbk = (unsigned)((warps + 7) / 8);
+    const size_t sm = (D == 3) ? win_smem<3>(8) : win_smem<2>(8);
+    const double invh = 1.0 / s->h;
+    const double invhd = (D == 3) ? invh * invh * invh : invh * invh;
+    const double two_rho = 2.0 / s->rho;
+    const bool kp = top->debug_keep_f != 0;
+    const int z0 = PART ? (int)s->z0 : 0, nzl = PART ? (int)s->nl : 0;
+#define IBGM_SW(Dd, K, KP)                                                                                  \
+    do {                                                                                                    \
+        const cudaError_t ae_ = box_attr<200 + 10 * Dd + 4 * K + 2 * KP + PART>(k_spread_win<Dd, K, KP, PART>, sm); \
+        if (ae_ != cudaSuccess) return ae_;                                                                 \
+        k_spread_win<Dd, K, KP, PART><<<nbk, 256, sm, s->stream>>>(top->Xh, top->F, top->wgt, s->nprev[0],  \
+                s->nprev[1], s->nprev[2], s->f[0], s->f[1], s->f[2], top->npts, (int)s->n, invh, invhd, two_rho, \
+                list, count, z0, nzl);                                                                      \
+    } while (0)
+    if (D == 2) {
+        if (top->kernel == IB_DELTA_COS4) { if (kp) IBGM_SW(2, 0, true); else IBGM_SW(2, 0, false); }
+        else { if (kp) IBGM_SW(2, 1, true); else IBGM_SW(2, 1, false); }
+    } else {
+        if (top->kernel == IB_DELTA_COS4) { if (kp) IBGM_SW(3, 0, true); else IBGM_SW(3, 0, false); }
+        else { if (kp) IBGM_SW(3, 1, true); else IBGM_SW(3, 1, false); }
+    }
+#undef IBGM_SW
+    s->launches++;
+    return cudaGetLastError();
+}
+
 cudaError_t launch_spread(Ctx* s)
 {
     if (s->npts == 0) return cudaSuccess;
+    // auto in 3D: window-staged (config 4 spread 354 -> 264 us, 4.854 -> 4.759 ms/step;
+    // config 3 0.1727 -> 0.1709 ms/step); 2D keeps the quad-lane kernel (config 2:
+    // 8.1 us vs 12.8 window-staged -- a curve gives short windows little overlap)
+    if (s->spread_mode == 6 || (s->spread_mode == 0 && s->dim == 3)) return launch_spread_win<false>(s, s, nullptr, nullptr);
     // 0 (auto) and 4: quad-lane atomics; 1: per-point atomics; 2: brick-binned; 3: box-staged
-    if (s->spread_mode == 0 || s->spread_mode == 4 || s->spread_mode == 5) return launch_spread_quad(s);
+    if (s->spread_mode == 0 || s->spread_mode == 4 || s->spread_mode == 5) return launch_spread_quad(s);   // 0: 2D
     if (s->spread_mode == 3) return launch_spread_box(s);
     if (s->spread_mode == 1) return launch_spread_direct(s);
     const int thr = 256;

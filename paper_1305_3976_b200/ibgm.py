@@ -270,8 +270,9 @@ class Context:
 
     def set_debug(self, keep_f: bool, spread_mode: int = 0, interp_mode: int = 0):
         """keep_f: keep f^{n+1/2} for aux(); spread_mode: 0 auto, 1 per-point, 2 brick-binned,
-        3 box-staged, 4 quad-lane, 5 quad-lane with warp pre-reduction; interp_mode: 0 auto,
-        1 per-point, 2 box-staged, 3 quad-lane, 4 per (point, component)."""
+        3 box-staged, 4 quad-lane, 5 quad-lane with warp pre-reduction, 6 window-staged;
+        interp_mode: 0 auto, 1 per-point, 2 box-staged, 3 quad-lane, 4 per (point, component),
+        5 window-staged."""
         _ck(lib().ib_set_debug(self._h, int(keep_f) | (int(spread_mode) << 1) | (int(interp_mode) << 4)))
 
     def set_profiling(self, on: bool):

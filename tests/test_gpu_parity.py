@@ -83,11 +83,11 @@ def test_line_solve_full_size_sampled_3d_384():
 # ------------------------------------------------------------------ one step, per stage
 @pytest.mark.parametrize("cfg,over", [(0, {}), (1, dict(n=64, pts=256)), (3, dict(n=32, nodes=2000)),
                                       (4, dict(n=48, nodes=1500)), (2, dict(n=128, pts=512))])
-@pytest.mark.parametrize("spread_mode,interp_mode", [(1, 1), (2, 2), (3, 3), (4, 0), (5, 3), (5, 4)])
+@pytest.mark.parametrize("spread_mode,interp_mode", [(1, 1), (2, 2), (3, 3), (4, 0), (5, 3), (5, 4), (6, 4), (6, 5), (4, 5)])
 def test_one_step_stage_parity(cfg, over, spread_mode, interp_mode):
     """After one step: X^{n+1/2}, F^{n+1/2}, spread f, N(u^n), then u, p, psi, X -- with
     every spreading method (per-point, brick-binned, box-staged, quad-lane, quad-lane with
-    warp pre-reduction) and every
+    warp pre-reduction, window-staged) and every
     interpolation path (per-point, box-staged, quad-lane, per (point, component))."""
     from paper_1305_3976_b200 import inputs
     pr = inputs.config(cfg, **over)
@@ -115,7 +115,8 @@ def test_one_step_stage_parity(cfg, over, spread_mode, interp_mode):
 # ------------------------------------------------------------------ 10 steps, configs
 @pytest.mark.parametrize("cfg,over,mode", [(0, {}, 0), (1, {}, 0), (2, {}, 0), (3, {}, 0), (3, {}, 2), (3, {}, 1),
                                            (4, dict(n=96, nodes=4000), 0), (4, dict(n=96, nodes=4000), 2),
-                                           (4, dict(n=96, nodes=4000), 5),
+                                           (4, dict(n=96, nodes=4000), 5), (4, dict(n=96, nodes=4000), 6),
+                                           (2, {}, 6), (3, {}, 6),
                                            (2, dict(n=128, pts=256, kernel=1), 0)])
 def test_ten_step_parity(cfg, over, mode):
     """End-to-end bar of the north_star: rel L_inf <= 1e-9 on u, p and X after 10 steps.
@@ -246,15 +247,15 @@ def test_step_before_set_fields_is_an_error():
 
 
 def test_debug_flags_out_of_range_are_rejected():
-    """ib_set_debug: spreading method > 5, interpolation method > 4 or unknown bits are
+    """ib_set_debug: spreading method > 6, interpolation method > 5 or unknown bits are
     IB_EINVAL (include/ibgm.h), and leave the context usable."""
     from paper_1305_3976_b200 import ibgm
     ctx = ibgm.Context(2, 32, 0.01, 1.0, 1e-3)
-    for spread, interp in ((6, 0), (7, 0), (0, 5), (0, 7)):
+    for spread, interp in ((7, 0), (0, 6), (0, 7)):
         with pytest.raises(ibgm.IBGMError) as e:
             ctx.set_debug(False, spread, interp)
         assert e.value.code == -1
-    ctx.set_debug(False, 5, 4)
+    ctx.set_debug(False, 6, 4)
     ctx.set_fields(np.zeros((32, 32)), np.zeros((32, 32)))
     ctx.step(1)
     ctx.close()

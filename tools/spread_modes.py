@@ -42,5 +42,5 @@ if __name__ == "__main__":
     for cfg in [int(a) for a in sys.argv[1:]] or [3, 4]:
         for sm in [int(x) for x in os.environ.get("SPREAD_MODES", "0,4,5").split(",")]:
             print(json.dumps(run(cfg, sm, 0)), flush=True)
-        for im in ():
+        for im in [int(x) for x in os.environ.get("INTERP_MODES", "").split(",") if x]:
             print(json.dumps(run(cfg, 0, im)), flush=True)
