@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <climits>
+#include <cstdlib>
 
 #include "ibgm_internal.cuh"
 
@@ -1128,7 +1129,7 @@ __global__ void __launch_bounds__(256) k_spread_win(const double* __restrict__ X
     }
     const int nv = __popc(__ballot_sync(0xffffffffu, valid));  // valid lanes are a prefix
     const size_t nn = (size_t)n;
-    int bl[CPW][3], o[CPW][3], e[CPW][3], V[CPW];
+    int bl[CPW][3], o[CPW][3], e[CPW][3], V[CPW], myrel[CPW];
     double w[CPW][3][4];
     bool fits[CPW];
 #pragma unroll
@@ -1141,32 +1142,47 @@ __global__ void __launch_bounds__(256) k_spread_win(const double* __restrict__ X
 #pragma unroll
         for (int m = 0; m < 4; ++m) w[q][0][m] *= Fs;
         fits[q] = win_box<DIM, CAP>(bl[q], valid, n, o[q], e[q], V[q]);
+        myrel[q] = -1;
         if (fits[q]) {
             double* R = rec + (q * 32 + lane) * REC;
 #pragma unroll
             for (int a = 0; a < DIM; ++a)
 #pragma unroll
-                for (int m = 0; m < 4; ++m) R[4 * a + m] = w[q][a][m];
-            rel[q * 32 + lane] = (bl[q][0] - o[q][0]) + e[q][0] * ((bl[q][1] - o[q][1]) +
-                                                                 (DIM == 3 ? e[q][1] * (bl[q][2] - o[q][2]) : 0));
+                for (int m = 0; m < 4; ++m) R[4 * a + ((a == 2) ? ((m & 1) * 2 + (m >> 1)) : m)] = w[q][a][m];
+            myrel[q] = valid ? (bl[q][0] - o[q][0]) + e[q][0] * ((bl[q][1] - o[q][1]) +
+                                                               (DIM == 3 ? e[q][1] * (bl[q][2] - o[q][2]) : 0)) : -1;
+            rel[q * 32 + lane] = myrel[q];
             for (int i = lane; i < V[q]; i += 32) box[q * CAP + i] = 0.0;
         }
     }
     __syncwarp();
-    // accumulate: point by point, the lanes own distinct nodes of its support
+    // accumulate: the lanes own distinct nodes of a support.  3D: the window's points are
+    // taken in groups with the same base node (ballot), whose contributions to the lane's
+    // two nodes sum in registers; one read-modify-write of the box per group (a window of
+    // 32 points has ~9 distinct base nodes at config 4).  The record holds w_z as
+    // (w0, w2, w1, w3): lane dz reads its pair (w_dz, w_dz+2) with one 16-byte load.
     if (DIM == 3) {
         if (fits[0]) {
             const int dx = lane & 3, dy = (lane >> 2) & 3, dz = lane >> 4;
             const int e01 = e[0][0] * e[0][1];
             const int loff = dx + e[0][0] * dy + e01 * dz;
             const int st2 = 2 * e01;
-            for (int p = 0; p < nv; ++p) {
-                const double* R = rec + p * REC;
-                const int r = rel[p] + loff;
-                const double a = R[dx] * R[4 + dy];
-                const double v0 = a * R[8 + dz], v1 = a * R[10 + dz];
-                box[r] += v0;
-                box[r + st2] += v1;
+            unsigned pend = __ballot_sync(0xffffffffu, valid);
+            while (pend) {
+                const int p0 = __ffs(pend) - 1;
+                const int r0 = __shfl_sync(0xffffffffu, myrel[0], p0);
+                const unsigned grp = __ballot_sync(0xffffffffu, myrel[0] == r0) & pend;
+                pend &= ~grp;
+                double a0 = 0.0, a1 = 0.0;
+                for (unsigned g = grp; g; g &= g - 1) {
+                    const double* R = rec + (__ffs(g) - 1) * REC;
+                    const double2 wz = *reinterpret_cast<const double2*>(R + 8 + 2 * dz);
+                    const double a = R[dx] * R[4 + dy];
+                    a0 = fma(a, wz.x, a0);
+                    a1 = fma(a, wz.y, a1);
+                }
+                box[r0 + loff] += a0;
+                box[r0 + loff + st2] += a1;
                 __syncwarp();
             }
         }
@@ -1709,9 +1725,15 @@ template <bool PART>
 static cudaError_t launch_spread_win(Ctx* top, Ctx* s, const int* list, const int* count)
 {
     const int D = s->dim;
+    static int wpb = -1;             // warps per block (IBGM_WIN_WPB, A/B)
+    if (wpb < 0) {
+        const char* ev = getenv("IBGM_WIN_WPB");
+        wpb = ev ? atoi(ev) : 8;
+        if (wpb < 1 || wpb > 8) wpb = 8;
+    }
     const int64_t warps = ((top->npts + 31) / 32) * (D == 3 ? 3 : 1);
-    const unsigned nbk = (unsigned)((warps + 7) / 8);
-    const size_t sm = (D == 3) ? win_smem<3>(8) : win_smem<2>(8);
+    const unsigned nbk = (unsigned)((warps + wpb - 1) / wpb);
+    const size_t sm = (D == 3) ? win_smem<3>(wpb) : win_smem<2>(wpb);
     const double invh = 1.0 / s->h;
     const double invhd = (D == 3) ? invh * invh * invh : invh * invh;
     const double two_rho = 2.0 / s->rho;
@@ -1721,7 +1743,7 @@ static cudaError_t launch_spread_win(Ctx* top, Ctx* s, const int* list, const in
     do {                                                                                                    \
         const cudaError_t ae_ = box_attr<200 + 10 * Dd + 4 * K + 2 * KP + PART>(k_spread_win<Dd, K, KP, PART>, sm); \
         if (ae_ != cudaSuccess) return ae_;                                                                 \
-        k_spread_win<Dd, K, KP, PART><<<nbk, 256, sm, s->stream>>>(top->Xh, top->F, top->wgt, s->nprev[0],  \
+        k_spread_win<Dd, K, KP, PART><<<nbk, 32 * wpb, sm, s->stream>>>(top->Xh, top->F, top->wgt, s->nprev[0],  \
                 s->nprev[1], s->nprev[2], s->f[0], s->f[1], s->f[2], top->npts, (int)s->n, invh, invhd, two_rho, \
                 list, count, z0, nzl);                                                                      \
     } while (0)
