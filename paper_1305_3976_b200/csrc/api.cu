@@ -770,7 +770,8 @@ int ib_set_boundary(ib_ctx* c, int64_t npts, const double* X, int64_t nedges, co
         CKC(cudaMalloc(&G->Ured, sizeof(double) * cnt));
         CKC(cudaMemsetAsync(G->Upart, 0, sizeof(double) * cnt * slots, s->stream));
         G->ucap = cnt;
-        for (int r = 0; r < G->nloc; ++r) CKC(cudaMalloc(&G->sel[r], sizeof(int) * npts));
+        // (k_slab_select appends warp-aligned 32-slot chunks: up to npts rounded up to its 128-thread blocks)
+        for (int r = 0; r < G->nloc; ++r) CKC(cudaMalloc(&G->sel[r], sizeof(int) * (size_t)((npts + 127) / 128 * 128)));
         CKC(cudaMalloc(&G->sel_cnt, sizeof(int) * G->nloc));
     }
     CKC(cudaStreamSynchronize(s->stream));

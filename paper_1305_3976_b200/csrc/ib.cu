@@ -939,11 +939,18 @@ __global__ void __launch_bounds__(256) k_spread_quad(const double* __restrict__ 
     const int c = rem >> 3;
     const int64_t item = blk * 8 + (rem & 7);
     const int64_t nitem = PART ? (int64_t)*count : npts;
-    const bool valid = item < nitem;
+    bool valid = item < nitem;
     if (PART && blk * 8 >= nitem) return;  // the whole warp is past the list
     if (!red && !valid) return;
     int64_t k = valid ? item : nitem - 1;  // red: every lane takes part in the shuffles
-    if (PART) k = list[k];
+    if (PART) {
+        k = list[k];
+        if (k < 0) {                        // padding of a warp-aligned chunk (k_slab_select)
+            if (!red) return;
+            k = 0;
+            valid = false;
+        }
+    }
     double Xk[3] = {0, 0, 0};
 #pragma unroll
     for (int a = 0; a < DIM; ++a) Xk[a] = Xh[k * DIM + a];
@@ -1117,9 +1124,12 @@ __global__ void __launch_bounds__(256) k_spread_win(const double* __restrict__ X
     const int64_t nitem = PART ? (int64_t)*count : npts;
     if (win * 32 >= nitem) return;                              // warp-uniform
     const int64_t item = win * 32 + lane;
-    const bool valid = item < nitem;
+    bool valid = item < nitem;
     int64_t k = valid ? item : 0;
-    if (PART && valid) k = list[item];
+    if (PART && valid) {
+        k = list[item];
+        if (k < 0) { valid = false; k = 0; }     // padding of a warp-aligned chunk (k_slab_select)
+    }
     double Xk[3] = {0, 0, 0};
     double ws = 0.0;
     if (valid) {
@@ -1127,7 +1137,6 @@ __global__ void __launch_bounds__(256) k_spread_win(const double* __restrict__ X
         for (int a = 0; a < DIM; ++a) Xk[a] = Xh[k * DIM + a];
         ws = wgt[k] * invhd;
     }
-    const int nv = __popc(__ballot_sync(0xffffffffu, valid));  // valid lanes are a prefix
     const size_t nn = (size_t)n;
     int bl[CPW][3], o[CPW][3], e[CPW][3], V[CPW], myrel[CPW];
     double w[CPW][3][4];
@@ -1195,10 +1204,11 @@ __global__ void __launch_bounds__(256) k_spread_win(const double* __restrict__ X
         double* bh = box + h * CAP;
         const double* rh = rec + h * 32 * REC;
         const int* relh = rel + h * 32;
-        for (int p = 0; p < nv; ++p) {
-            if (fh) {
+        for (int p = 0; p < 32; ++p) {
+            const int r = relh[p];                      // -1: no point in this lane
+            if (fh && r >= 0) {
                 const double* R = rh + p * REC;
-                bh[relh[p] + loff] += R[dx] * R[4 + dy];
+                bh[r + loff] += R[dx] * R[4 + dy];
             }
             __syncwarp();
         }
@@ -1267,12 +1277,17 @@ __global__ void __launch_bounds__(256) k_spread_win(const double* __restrict__ X
 // components (warp = window x component); the block barrier orders every read of X^n
 // before the writes of X^{n+1} (all components of a point are in the block).  2D: a warp
 // = one window, both components (boxes [2][CAP]), each lane owns one point.
-template <int DIM, int KER>
+// PART (z-slab, slab.cu): the items are the listed points (warp-aligned chunks, -1 =
+// none), the box holds only the nodes of this slab's planes z0 .. z0+nzl-1 (0 elsewhere),
+// and the partial sums go to Upart (U^n = their sum over the slabs; no Steps 1b-1c).
+template <int DIM, int KER, bool PART>
 __global__ void __launch_bounds__(256) k_interp_win(const double* __restrict__ u0, const double* __restrict__ u1,
                                                     const double* __restrict__ u2, double* __restrict__ X,
                                                     double* __restrict__ Xh, double* __restrict__ Uprev,
                                                     double* __restrict__ Xold, double* __restrict__ Uold,
-                                                    int64_t npts, int n, double invh, double dt, int first)
+                                                    int64_t npts, int n, double invh, double dt, int first,
+                                                    double* __restrict__ Upart, const int* __restrict__ list,
+                                                    const int* __restrict__ count, int z0, int nzl)
 {
     using W = WinCfg<DIM>;
     constexpr int CPW = W::CPW, CAP = W::CAP;
@@ -1282,14 +1297,20 @@ __global__ void __launch_bounds__(256) k_interp_win(const double* __restrict__ u
     const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t win = gw / W::WPW;
     const int cw = (int)(gw - win * W::WPW);
-    const int64_t k = win * 32 + lane;
-    const bool valid = k < npts;
+    const int64_t nitem = PART ? (int64_t)*count : npts;
+    const int64_t item = win * 32 + lane;
+    bool valid = item < nitem;
+    int64_t k = item;
+    if (PART && valid) {
+        k = list[item];
+        valid = k >= 0;
+    }
     double Xk[3] = {0, 0, 0};
     if (valid)
 #pragma unroll
         for (int a = 0; a < DIM; ++a) Xk[a] = X[k * DIM + a];
-    if (DIM == 3) __syncthreads();     // every X^n read of the block precedes any X^{n+1} write
-    if (win * 32 >= npts) return;      // warp-uniform
+    if (DIM == 3 && !PART) __syncthreads();   // every X^n read of the block precedes any X^{n+1} write
+    if (win * 32 >= nitem) return;            // warp-uniform
     const size_t nn = (size_t)n;
 #pragma unroll
     for (int q = 0; q < CPW; ++q) {
@@ -1315,7 +1336,14 @@ __global__ void __launch_bounds__(256) k_interp_win(const double* __restrict__ u
                 if (gx >= n) gx -= n;
                 if (gy >= n) gy -= n;
                 if (gz >= n) gz -= n;
-                bq[i] = __ldg(uc + ((DIM == 3) ? nn * (nn * (size_t)gz + gy) + gx : nn * (size_t)gy + gx));
+                if (PART) {
+                    const int l = ((DIM == 3) ? gz : gy) - z0;      // local plane of the last axis
+                    bq[i] = ((unsigned)l < (unsigned)nzl)
+                                ? __ldg(uc + ((DIM == 3) ? nn * (nn * (size_t)l + gy) + gx : nn * (size_t)l + gx))
+                                : 0.0;
+                } else {
+                    bq[i] = __ldg(uc + ((DIM == 3) ? nn * (nn * (size_t)gz + gy) + gx : nn * (size_t)gy + gx));
+                }
             }
             __syncwarp();
             if (valid) {
@@ -1344,11 +1372,21 @@ __global__ void __launch_bounds__(256) k_interp_win(const double* __restrict__ u
             const int m2n = (DIM == 3) ? 4 : 1;
 #pragma unroll
             for (int m2 = 0; m2 < m2n; ++m2) {
-                const size_t pl = (DIM == 3) ? nn * nn * (size_t)wrap1(wb[2] + m2, n) : 0;
+                int lz = (DIM == 3) ? wrap1(wb[2] + m2, n) : 0;
+                if (PART && DIM == 3) {
+                    lz -= z0;
+                    if ((unsigned)lz >= (unsigned)nzl) continue;
+                }
+                const size_t pl = (DIM == 3) ? nn * nn * (size_t)lz : 0;
                 double pa = 0.0;
 #pragma unroll
                 for (int m1 = 0; m1 < 4; ++m1) {
-                    const size_t row = pl + nn * (size_t)wrap1(wb[1] + m1, n);
+                    int ly = wrap1(wb[1] + m1, n);
+                    if (PART && DIM == 2) {
+                        ly -= z0;
+                        if ((unsigned)ly >= (unsigned)nzl) continue;
+                    }
+                    const size_t row = pl + nn * (size_t)ly;
                     double r = 0.0;
 #pragma unroll
                     for (int m0 = 0; m0 < 4; ++m0) r += w[0][m0] * __ldg(uc + row + wrap1(wb[0] + m0, n));
@@ -1357,7 +1395,9 @@ __global__ void __launch_bounds__(256) k_interp_win(const double* __restrict__ u
                 acc += (DIM == 3) ? w[2][m2] * pa : pa;
             }
         }
-        if (valid) {
+        if (PART) {
+            if (valid) Upart[k * DIM + c] = acc;
+        } else if (valid) {
             // Steps 1b-1c for component c of this point
             const double xc = (c == 0) ? Xk[0] : (c == 1 ? Xk[1] : Xk[2]);
             const double up = Uprev[k * DIM + c];
@@ -1386,6 +1426,7 @@ __global__ void __launch_bounds__(64 * DIM) k_interp_comp_part(const double* __r
     const int64_t i = blockIdx.x * 64LL + (threadIdx.x & 63);
     if (i >= *count) return;
     const int64_t k = list[i];
+    if (k < 0) return;                  // padding of a warp-aligned chunk (k_slab_select)
     const double* uc = (c == 0) ? u0 : (c == 1 ? u1 : u2);
     const size_t nn = (size_t)n;
     int b[3] = {0, 0, 0};
@@ -1421,9 +1462,33 @@ __global__ void __launch_bounds__(64 * DIM) k_interp_comp_part(const double* __r
     Upart[k * DIM + c] = acc;
 }
 
+// list capacity of a slab selection: npts rounded up to k_slab_select's 128-thread blocks
+static int64_t sel_cap(int64_t npts) { return (npts + 127) / 128 * 128; }
+
+template <int ID, class K>
+static cudaError_t box_attr(K kern, size_t sm);
+
 cudaError_t launch_interp_part(Ctx* top, Ctx* s, double* Upart, const int* list, const int* count)
 {
-    const unsigned nb = (unsigned)((top->npts + 63) / 64);
+    if (s->dim == 3) {
+        // window-staged (as on one GPU): 6 warps = 2 windows x 3 components per block
+        const int64_t warps = ((sel_cap(top->npts) + 31) / 32) * 3;
+        const unsigned nbk = (unsigned)((warps + 5) / 6);
+        const size_t sm = (size_t)6 * WinCfg<3>::CAP * sizeof(double);
+        const double invh = 1.0 / s->h;
+#define IBGM_IWP(K)                                                                                          \
+    do {                                                                                                     \
+        const cudaError_t ae_ = box_attr<330 + K>(k_interp_win<3, K, true>, sm);                             \
+        if (ae_ != cudaSuccess) return ae_;                                                                  \
+        k_interp_win<3, K, true><<<nbk, 192, sm, s->stream>>>(s->u[0], s->u[1], s->u[2], top->X, nullptr,   \
+                nullptr, nullptr, nullptr, top->npts, (int)s->n, invh, 0.0, 0, Upart, list, count, (int)s->z0, (int)s->nl); \
+    } while (0)
+        if (top->kernel == IB_DELTA_COS4) IBGM_IWP(0); else IBGM_IWP(1);
+#undef IBGM_IWP
+        s->launches++;
+        return cudaGetLastError();
+    }
+    const unsigned nb = (unsigned)((sel_cap(top->npts) + 63) / 64);
     const double invh = 1.0 / s->h;
 #define IBGM_ICP(D, K) k_interp_comp_part<D, K><<<nb, 64 * D, 0, s->stream>>>(s->u[0], s->u[1], s->u[2], top->X, Upart, \
         list, count, (int)s->n, (int)s->z0, (int)s->nl, invh)
@@ -1440,7 +1505,7 @@ static cudaError_t launch_spread_win(Ctx* top, Ctx* s, const int* list, const in
 cudaError_t launch_spread_part(Ctx* top, Ctx* s, const int* list, const int* count)
 {
     if (s->dim == 3) return launch_spread_win<true>(top, s, list, count);
-    const int64_t thr = ((top->npts + 7) / 8) * 8 * s->dim * 4;
+    const int64_t thr = ((sel_cap(top->npts) + 7) / 8) * 8 * s->dim * 4;
     const unsigned nbk = (unsigned)((thr + 255) / 256);
     const double invh = 1.0 / s->h;
     const double invhd = (s->dim == 3) ? invh * invh * invh : invh * invh;
@@ -1523,10 +1588,10 @@ cudaError_t launch_interp_evolve(Ctx* s, int first)
         const double invh = 1.0 / s->h;
 #define IBGM_IW(Dd, K)                                                                                           \
     do {                                                                                                         \
-        const cudaError_t ae_ = box_attr<300 + 10 * Dd + K>(k_interp_win<Dd, K>, sm);                           \
+        const cudaError_t ae_ = box_attr<300 + 10 * Dd + K>(k_interp_win<Dd, K, false>, sm);                    \
         if (ae_ != cudaSuccess) return ae_;                                                                      \
-        k_interp_win<Dd, K><<<nbk, 32 * wpb, sm, s->stream>>>(s->u[0], s->u[1], s->u[2], s->X, s->Xh, s->Uprev, \
-                                                             s->Xold, s->Uold, s->npts, (int)s->n, invh, s->dt, first); \
+        k_interp_win<Dd, K, false><<<nbk, 32 * wpb, sm, s->stream>>>(s->u[0], s->u[1], s->u[2], s->X, s->Xh,     \
+                s->Uprev, s->Xold, s->Uold, s->npts, (int)s->n, invh, s->dt, first, nullptr, nullptr, nullptr, 0, 0); \
     } while (0)
         if (D == 2) { if (s->kernel == IB_DELTA_COS4) IBGM_IW(2, 0); else IBGM_IW(2, 1); }
         else { if (s->kernel == IB_DELTA_COS4) IBGM_IW(3, 0); else IBGM_IW(3, 1); }
@@ -1731,7 +1796,8 @@ static cudaError_t launch_spread_win(Ctx* top, Ctx* s, const int* list, const in
         wpb = ev ? atoi(ev) : 8;
         if (wpb < 1 || wpb > 8) wpb = 8;
     }
-    const int64_t warps = ((top->npts + 31) / 32) * (D == 3 ? 3 : 1);
+    const int64_t items = PART ? sel_cap(top->npts) : top->npts;
+    const int64_t warps = ((items + 31) / 32) * (D == 3 ? 3 : 1);
     const unsigned nbk = (unsigned)((warps + wpb - 1) / wpb);
     const size_t sm = (D == 3) ? win_smem<3>(wpb) : win_smem<2>(wpb);
     const double invh = 1.0 / s->h;

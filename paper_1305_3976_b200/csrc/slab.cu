@@ -602,14 +602,16 @@ __global__ void k_slab_select(const double* __restrict__ X, long long npts, int 
             hit = hit || (unsigned)(g - z0) < (unsigned)nz;
         }
     }
+    // a warp with any hit appends one 32-slot chunk in its own (Morton) order, -1 where
+    // a lane has no hit: a window of 32 list entries is then one source warp's points
+    // (spatially compact for the window-staged IB kernels), wherever the chunk lands
     const unsigned m = __ballot_sync(0xffffffffu, hit);
     if (m == 0) return;
     const int lane = threadIdx.x & 31;
-    const int leader = __ffs(m) - 1;
     int base = 0;
-    if (lane == leader) base = atomicAdd(count, __popc(m));
-    base = __shfl_sync(0xffffffffu, base, leader);
-    if (hit) list[base + __popc(m & ((1u << lane) - 1u))] = (int)k;
+    if (lane == 0) base = atomicAdd(count, 32);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    list[base + lane] = hit ? (int)k : -1;
 }
 
 template <int DIM, int KER>
@@ -621,6 +623,7 @@ __global__ void k_interp_part(const double* __restrict__ u0, const double* __res
     const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i >= *count) return;
     const long long k = list[i];
+    if (k < 0) return;                  // padding of a warp-aligned chunk (k_slab_select)
     double Xk[3];
 #pragma unroll
     for (int a = 0; a < DIM; ++a) Xk[a] = X[k * DIM + a];
@@ -696,6 +699,7 @@ __global__ void __launch_bounds__(128) k_spread_part(const double* __restrict__ 
     const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i >= *count) return;
     const long long k = list[i];
+    if (k < 0) return;                  // padding of a warp-aligned chunk (k_slab_select)
     double Xk[3];
 #pragma unroll
     for (int a = 0; a < DIM; ++a) Xk[a] = Xh[k * DIM + a];
@@ -779,7 +783,7 @@ cudaError_t slab_interp_part(Ctx* top, Ctx* s, double* Upart, int* list, int* co
     if (e != cudaSuccess) return e;
     if ((e = slab_select(top, s, top->X, list, count)) != cudaSuccess) return e;
     if (slab_ib_fast()) return launch_interp_part(top, s, Upart, list, count);
-#define IBGM_IP(D, K) k_interp_part<D, K><<<nb128(top->npts), 128, 0, s->stream>>>( \
+#define IBGM_IP(D, K) k_interp_part<D, K><<<nb128(nb128(top->npts) * 128LL), 128, 0, s->stream>>>( \
         s->u[0], s->u[1], s->u[2], top->X, Upart, list, count, (int)s->n, (int)s->z0, (int)s->nl, invh)
     if (s->dim == 2) { if (top->kernel == IB_DELTA_COS4) IBGM_IP(2, 0); else IBGM_IP(2, 1); }
     else { if (top->kernel == IB_DELTA_COS4) IBGM_IP(3, 0); else IBGM_IP(3, 1); }
@@ -813,7 +817,7 @@ cudaError_t slab_spread_part(Ctx* top, Ctx* s, int* list, int* count)
     cudaError_t e = slab_select(top, s, top->Xh, list, count);
     if (e != cudaSuccess) return e;
     if (slab_ib_fast()) return launch_spread_part(top, s, list, count);
-#define IBGM_SPP(D, K, KP) k_spread_part<D, K, KP><<<nb128(top->npts), 128, 0, s->stream>>>(                  \
+#define IBGM_SPP(D, K, KP) k_spread_part<D, K, KP><<<nb128(nb128(top->npts) * 128LL), 128, 0, s->stream>>>(                  \
         top->Xh, top->F, top->wgt, s->nprev[0], s->nprev[1], s->nprev[2], s->f[0], s->f[1], s->f[2], list, count, \
         (int)s->n, (int)s->z0, (int)s->nl, invh, invhd, 2.0 / s->rho)
     if (s->dim == 2) {
