@@ -165,6 +165,25 @@ void make_line_coef(LineCoef* C, SchurInv* SI, int64_t N, int L, double c_, doub
         for (int q = 0; q < F.P; ++q) SI->sinvT[q * F.P + p] = SI->sinv[p * F.P + q];
     C->inv_n = (double)(1.0L / (long double)N);
     for (int q = 0; q < F.P; ++q) SI->colsum[q] = (double)F.colsum[q];
+    // banded S^{-1} (LineCoef::band): circulant to rounding, and negligible beyond the band
+    // (A/B switch: IBGM_BAND=0 keeps the dense product)
+    C->band = -1;
+    const int P = F.P;
+    const long double ref = fabsl(F.sinv[0]);
+    const char* eb = getenv("IBGM_BAND");
+    bool circ = P > 1 && ref > 0 && !(eb && atoi(eb) == 0);
+    for (int p = 0; p < P && circ; ++p)
+        for (int q = 0; q < P; ++q)
+            if (fabsl(F.sinv[p * P + q] - F.sinv[(q - p + P) % P]) > 1e-14L * ref) { circ = false; break; }
+    for (int bw = 0; circ && bw <= kMaxBand && 2 * bw + 1 < P; ++bw) {
+        long double out = 0;
+        for (int d = bw + 1; d <= P - 1 - bw; ++d) out = std::max(out, fabsl(F.sinv[d]));
+        if (out <= 1e-18L * ref) {
+            C->band = bw;
+            for (int d = -bw; d <= bw; ++d) C->w[kMaxBand + d] = (double)F.sinv[(d + P) % P];
+            break;
+        }
+    }
 }
 
 // Slab coefficient block (layout in ibgm_internal.cuh): the same factors for a line of
@@ -874,6 +893,59 @@ static bool lookahead_on(const Ctx* s)
     return s->lookahead && slab_ok && s->npts > 0 && !s->profiling && !s->debug_keep_f;
 }
 
+// A captured step keeps the stream priorities as kernel-node priorities (the look-ahead
+// IB kernels were launched on the high-priority side stream), but a graph launch runs
+// every node at the priority of the stream it is launched into unless instantiated
+// with cudaGraphInstantiateFlagUseNodePriority.  IBGM_NODE_PRIO selects:
+//   0 (default) the launch stream's priority for every node;
+//   1 the captured priorities (IB look-ahead above the psi passes);
+//   2 as 1, and list the kernel nodes with their priorities on stderr;
+//   3 inverted (the psi passes above the IB look-ahead).
+// Measured (graph ms/step, config 4 / config 3): 0: 4.643-4.672 / 0.1623-0.1638;
+// 1: 4.849 / 0.1638; 3: 4.663 / 0.1711 -- the block scheduler's default interleaving wins.
+static cudaError_t instantiate_step_graph(Ctx* s, cudaGraph_t g, cudaGraphExec_t* ge)
+{
+    (void)s;
+    const char* e = getenv("IBGM_NODE_PRIO");
+    const int mode = e ? atoi(e) : 0;
+    if (mode == 3) {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        size_t nn = 0;
+        cudaGraphGetNodes(g, nullptr, &nn);
+        std::vector<cudaGraphNode_t> nodes(nn);
+        cudaGraphGetNodes(g, nodes.data(), &nn);
+        for (size_t i = 0; i < nn; ++i) {
+            cudaGraphNodeType t;
+            cudaGraphNodeGetType(nodes[i], &t);
+            if (t != cudaGraphNodeTypeKernel) continue;
+            cudaLaunchAttributeValue v{};
+            cudaGraphKernelNodeGetAttribute(nodes[i], cudaLaunchAttributePriority, &v);
+            v.priority = (v.priority == hi) ? lo : hi;
+            cudaGraphKernelNodeSetAttribute(nodes[i], cudaLaunchAttributePriority, &v);
+        }
+    }
+    if (mode == 2) {
+        size_t nn = 0;
+        cudaGraphGetNodes(g, nullptr, &nn);
+        std::vector<cudaGraphNode_t> nodes(nn);
+        cudaGraphGetNodes(g, nodes.data(), &nn);
+        for (size_t i = 0; i < nn; ++i) {
+            cudaGraphNodeType t;
+            cudaGraphNodeGetType(nodes[i], &t);
+            if (t != cudaGraphNodeTypeKernel) continue;
+            cudaLaunchAttributeValue v{};
+            cudaGraphKernelNodeGetAttribute(nodes[i], cudaLaunchAttributePriority, &v);
+            cudaKernelNodeParams kp{};
+            cudaGraphKernelNodeGetParams(nodes[i], &kp);
+            const char* nm = nullptr;
+            cudaFuncGetName(&nm, kp.func);
+            fprintf(stderr, "[ibgm] graph kernel node %zu prio %d %s\n", i, v.priority, nm ? nm : "?");
+        }
+    }
+    return cudaGraphInstantiateWithFlags(ge, g, mode ? cudaGraphInstantiateFlagUseNodePriority : 0);
+}
+
 // Steps 1-2 (interpolate + evolve, force, spread) on context view v
 static cudaError_t enqueue_ib(Ctx* v, int first)
 {
@@ -907,7 +979,7 @@ int ib_step(ib_ctx* c, int64_t nsteps)
                 cudaError_t ce = cudaStreamEndCapture(s->stream, &g);
                 if (rc != IB_OK) return rc;
                 CKC(ce);
-                CKC(cudaGraphInstantiate(&s->gexec[par], g, 0));
+                CKC(instantiate_step_graph(s, g, &s->gexec[par]));
                 cudaGraphDestroy(g);
                 s->gvalid[par] = true;
                 s->glaunches[par] = total_launches(s) - l0;

@@ -89,6 +89,29 @@ __device__ __forceinline__ double group_sum(double v, int P, int gbase)
     return t;
 }
 
+// y_s = (S^{-1} r)_s with r_q held by lane gbase + q: the banded circulant form when the
+// line's S^{-1} allows it (LineCoef::band), else the dense row s of S^{-1} (sinvT in
+// shared memory).  All 32 lanes must call it.
+__device__ __forceinline__ double schur_apply_lanes(const LineCoef& C, double r, int s, int P, int gbase,
+                                                    const double* __restrict__ sinvT)
+{
+    const int B = C.band;
+    if (B >= 0) {
+        double ys = C.w[kMaxBand] * r;
+#pragma unroll
+        for (int d = 1; d <= kMaxBand; ++d) {
+            if (d > B) break;
+            const int qp = (s + d >= P) ? s + d - P : s + d, qm = (s - d < 0) ? s - d + P : s - d;
+            ys = fma(C.w[kMaxBand + d], __shfl_sync(kFull, r, gbase + qp), ys);
+            ys = fma(C.w[kMaxBand - d], __shfl_sync(kFull, r, gbase + qm), ys);
+        }
+        return ys;
+    }
+    double ys = 0.0;
+    for (int q = 0; q < P; ++q) ys = fma(sinvT[q * P + s], __shfl_sync(kFull, r, gbase + q), ys);
+    return ys;
+}
+
 // -------------------------------------------------------------------------------
 // Warp-synchronous Schur-segmented solve of one part (L unknowns, rows sL..sL+L-1)
 // of a cyclic line whose P parts sit in lanes gbase .. gbase+P-1.  All 32 lanes of
@@ -119,8 +142,7 @@ __device__ __forceinline__ void ws_solve(double (&x)[L], const LineCoef& C, int 
     const double fl_prev = __shfl_sync(kFull, x[M], sprev);
     const double r = x[0] - c * fl_prev - b * x[1];
     // y = S^{-1} r  (S precomputed); this part needs y_p, y_{p+1}
-    double ys = 0.0;
-    for (int q = 0; q < P; ++q) ys = fma(sinvT[q * P + s], __shfl_sync(kFull, r, gbase + q), ys);
+    const double ys = schur_apply_lanes(C, r, s, P, gbase, sinvT);
     const double ys1 = __shfl_sync(kFull, ys, snext);
     // correction x_p = f*_p - B_p^{-1} E_p y, E_p y = c y_p e_1 + b y_{p+1} e_m
     x[0] = ys;
@@ -174,8 +196,7 @@ __device__ __forceinline__ void ws_solve_smem(double* x, const LineCoef& C, int 
     const int snext = gbase + ((s == P - 1) ? 0 : s + 1);
     const double fl_prev = __shfl_sync(kFull, x[M], sprev);
     const double r = x[0] - c * fl_prev - b * x[1];
-    double ys = 0.0;
-    for (int q = 0; q < P; ++q) ys = fma(sinvT[q * P + s], __shfl_sync(kFull, r, gbase + q), ys);
+    const double ys = schur_apply_lanes(C, r, s, P, gbase, sinvT);
     const double ys1 = __shfl_sync(kFull, ys, snext);
     x[0] = ys;
     const double cy = c * ys, by = b * ys1;
@@ -621,8 +642,11 @@ struct LinePass {
     }
 };
 
-__device__ __forceinline__ void load_sinvT(double* sinvT, const SchurInv* SI, int P)
+// (not needed when the line's S^{-1} is applied in banded form)
+__device__ __forceinline__ void load_sinvT(double* sinvT, const SchurInv* SI, const LineCoef& C)
 {
+    if (C.band >= 0) return;
+    const int P = C.P;
     for (int e = threadIdx.x; e < P * P; e += blockDim.x) sinvT[e] = SI->sinvT[e];
 }
 
@@ -638,7 +662,7 @@ __global__ void __launch_bounds__(256, MINB) k_lines(const LineCoef C, const Sch
     double* sinvT = smem;
     double* tile = smem + P * P;
     double* tile2 = tile + (size_t)NC * R * TP;   // LAST: u^n, PSI_LAST: q (prefetched with the fill)
-    load_sinvT(sinvT, SI, P);                     // line factors: not written by the predecessor
+    load_sinvT(sinvT, SI, C);                     // line factors: not written by the predecessor
     pdl_wait();
     pdl_trigger();
     const int comp = (NC == 1) ? blockIdx.z : 0;
@@ -673,7 +697,7 @@ __global__ void __launch_bounds__(32 * WPB, MINB) k_xwarp(const LineCoef C, cons
     double* sinvT = smem;
     double* tile = smem + P * P + (size_t)w * NT * NC * lpw * TP;
     double* tile2 = tile + (size_t)NC * lpw * TP;
-    load_sinvT(sinvT, SI, P);
+    load_sinvT(sinvT, SI, C);
     __syncthreads();
     const int g0 = (blockIdx.x * WPB + w) * lpw;
     const int nrow = (DIM == 2) ? A.nl : n;
@@ -709,7 +733,7 @@ __global__ void __launch_bounds__(512) k_strided(const LineCoef C, const SchurIn
     double* yb = rr + P * RI;            // [P][RI] y_s
     double* ds = yb + P * RI;            // [P][RI] line sums of d (mean correction)
     double* xs = ds + P * RI;            // [P][RI] line sums of x
-    load_sinvT(sinvT, SI, P);
+    load_sinvT(sinvT, SI, C);
     const int il = threadIdx.x % RI, s = threadIdx.x / RI;
     const int i = blockIdx.x * RI + il;
     const int comp = (KIND == K_DIVPSI) ? 0 : blockIdx.z;
@@ -772,7 +796,19 @@ __global__ void __launch_bounds__(512) k_strided(const LineCoef C, const SchurIn
     rr[s * RI + il] = x[0] - c * xl[sp * RI + il] - b * x[1];
     __syncthreads();
     double ys = 0.0;
-    for (int q = 0; q < P; ++q) ys = fma(sinvT[q * P + s], rr[q * RI + il], ys);
+    if (C.band >= 0) {
+        // banded circulant S^{-1} (LineCoef::band)
+        ys = C.w[kMaxBand] * rr[s * RI + il];
+#pragma unroll
+        for (int d = 1; d <= kMaxBand; ++d) {
+            if (d > C.band) break;
+            const int qp = (s + d >= P) ? s + d - P : s + d, qm = (s - d < 0) ? s - d + P : s - d;
+            ys = fma(C.w[kMaxBand + d], rr[qp * RI + il], ys);
+            ys = fma(C.w[kMaxBand - d], rr[qm * RI + il], ys);
+        }
+    } else {
+        for (int q = 0; q < P; ++q) ys = fma(sinvT[q * P + s], rr[q * RI + il], ys);
+    }
     yb[s * RI + il] = ys;
     __syncthreads();
     const double ys1 = yb[sn * RI + il];

@@ -13,6 +13,7 @@ namespace ibgm {
 
 constexpr int kMaxSeg = 32;   // max segments P per line (reduced Schur system size)
 constexpr int kMaxL = 32;     // max segment length L
+constexpr int kMaxBand = 4;   // max half-width of a banded S^{-1} (LineCoef::w)
 
 // Constant-coefficient cyclic tridiagonal system  c x_{i-1} + a x_i + b x_{i+1} = d_i
 // solved by the paper's Schur-complement splitting applied
@@ -32,6 +33,13 @@ struct LineCoef {
     double cp[kMaxL];         // Thomas: b/den_i
     double g[kMaxL];          // B^{-1} e_1   (first column of B^{-1})
     double h[kMaxL];          // B^{-1} e_m   (last column of B^{-1})
+    // S is circulant (P equal parts, constant coefficients), so S^{-1} is too.  When every
+    // entry of S^{-1} farther than `band` parts from the diagonal is below 1e-18 of the
+    // diagonal (well-conditioned viscous systems: the coupling between parts decays like
+    // lambda^L, lambda ~ kappa), y_s = sum_{|d| <= band} w[kMaxBand + d] r_{s+d} replaces the
+    // dense product; band = -1: dense S^{-1} (SchurInv).
+    int band;
+    double w[2 * kMaxBand + 1];
 };
 
 // dense inverse of the P x P periodic Schur matrix S and its column sums (device)

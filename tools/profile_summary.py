@@ -85,7 +85,9 @@ with open(os.path.join(out_dir, f"{tag}_ncu_full.txt"), "w") as f:
         grid = row[jx["Grid Size"]] if "Grid Size" in jx else ""
         ph = phase_of(nm, grid)
         g = lambda k: float(row[jx[k]].replace(",", ""))
-        us = g("gpu__time_duration.sum")
+        tu = r[1][jx["gpu__time_duration.sum"]].lower()
+        us = g("gpu__time_duration.sum") * {"ns": 1e-3, "nsecond": 1e-3, "ms": 1e3, "msecond": 1e3, "s": 1e6,
+                                             "second": 1e6}.get(tu, 1.0)
         rd, wr = g("dram__bytes_read.sum"), g("dram__bytes_write.sum")
         units = r[1]
         u = units[jx["dram__bytes_read.sum"]].lower()
