@@ -175,6 +175,13 @@ void make_line_coef(LineCoef* C, SchurInv* SI, int64_t N, int L, double c_, doub
     for (int p = 0; p < P && circ; ++p)
         for (int q = 0; q < P; ++q)
             if (fabsl(F.sinv[p * P + q] - F.sinv[(q - p + P) % P]) > 1e-14L * ref) { circ = false; break; }
+    {
+        // (A/B switch: IBGM_CIRC=0 stages the dense S^{-1} for the non-banded systems)
+        const char* ec = getenv("IBGM_CIRC");
+        C->circ = (circ && !(ec && atoi(ec) == 0)) ? 1 : 0;
+        if (C->circ)
+            for (int d = 0; d < P; ++d) C->wf[d] = (double)F.sinv[d];
+    }
     for (int bw = 0; circ && bw <= kMaxBand && 2 * bw + 1 < P; ++bw) {
         long double out = 0;
         for (int d = bw + 1; d <= P - 1 - bw; ++d) out = std::max(out, fabsl(F.sinv[d]));

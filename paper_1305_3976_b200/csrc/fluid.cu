@@ -89,14 +89,23 @@ __device__ __forceinline__ double group_sum(double v, int P, int gbase)
     return t;
 }
 
+// Which forms of y = S^{-1} r a pass compiles (MODES bit mask; the unused unrolled
+// forms cost instruction-cache space): viscous passes are banded, psi passes circulant.
+constexpr int kSchurBand = 1, kSchurCirc = 2;
+__host__ __device__ constexpr int schur_modes(int kind)
+{
+    return (kind == 0 || kind == 2) ? kSchurBand : ((kind == 3 || kind == 4) ? kSchurCirc : kSchurBand | kSchurCirc);
+}
+
 // y_s = (S^{-1} r)_s with r_q held by lane gbase + q: the banded circulant form when the
-// line's S^{-1} allows it (LineCoef::band), else the dense row s of S^{-1} (sinvT in
-// shared memory).  All 32 lanes must call it.
+// line's S^{-1} allows it (LineCoef::band), the full circulant row (LineCoef::circ), else
+// the dense row s of S^{-1} (sinvT in shared memory).  All 32 lanes must call it.
+template <int MODES>
 __device__ __forceinline__ double schur_apply_lanes(const LineCoef& C, double r, int s, int P, int gbase,
                                                     const double* __restrict__ sinvT)
 {
     const int B = C.band;
-    if (B >= 0) {
+    if ((MODES & kSchurBand) && B >= 0) {
         double ys = C.w[kMaxBand] * r;
 #pragma unroll
         for (int d = 1; d <= kMaxBand; ++d) {
@@ -108,6 +117,16 @@ __device__ __forceinline__ double schur_apply_lanes(const LineCoef& C, double r,
         return ys;
     }
     double ys = 0.0;
+    if ((MODES & kSchurCirc) && C.circ) {
+        // circulant: y_s = sum_d wf[d] r_{(s+d) mod P}, wf uniform across lanes
+#pragma unroll
+        for (int d = 0; d < kMaxSeg; ++d) {
+            if (d >= P) break;
+            const int q = (s + d >= P) ? s + d - P : s + d;
+            ys = fma(C.wf[d], __shfl_sync(kFull, r, gbase + q), ys);
+        }
+        return ys;
+    }
     for (int q = 0; q < P; ++q) ys = fma(sinvT[q * P + s], __shfl_sync(kFull, r, gbase + q), ys);
     return ys;
 }
@@ -117,7 +136,7 @@ __device__ __forceinline__ double schur_apply_lanes(const LineCoef& C, double r,
 // of a cyclic line whose P parts sit in lanes gbase .. gbase+P-1.  All 32 lanes of
 // the warp must call it.
 // -------------------------------------------------------------------------------
-template <int L>
+template <int L, int MODES>
 __device__ __forceinline__ void ws_solve(double (&x)[L], const LineCoef& C, int s, int P, int gbase,
                                          const double* __restrict__ sinvT)
 {
@@ -142,7 +161,7 @@ __device__ __forceinline__ void ws_solve(double (&x)[L], const LineCoef& C, int 
     const double fl_prev = __shfl_sync(kFull, x[M], sprev);
     const double r = x[0] - c * fl_prev - b * x[1];
     // y = S^{-1} r  (S precomputed); this part needs y_p, y_{p+1}
-    const double ys = schur_apply_lanes(C, r, s, P, gbase, sinvT);
+    const double ys = schur_apply_lanes<MODES>(C, r, s, P, gbase, sinvT);
     const double ys1 = __shfl_sync(kFull, ys, snext);
     // correction x_p = f*_p - B_p^{-1} E_p y, E_p y = c y_p e_1 + b y_{p+1} e_m
     x[0] = ys;
@@ -167,7 +186,7 @@ __device__ __forceinline__ void ws_solve(double (&x)[L], const LineCoef& C, int 
 // The same solve for long segments (L = 64, 128: 2D N = 2048, 4096), run directly on the
 // lane's segment of the shared tile (no register array) with the factors in C.ext.
 // -------------------------------------------------------------------------------
-template <int L>
+template <int L, int MODES>
 __device__ __forceinline__ void ws_solve_smem(double* x, const LineCoef& C, int s, int P, int gbase,
                                               const double* __restrict__ sinvT)
 {
@@ -196,7 +215,7 @@ __device__ __forceinline__ void ws_solve_smem(double* x, const LineCoef& C, int 
     const int snext = gbase + ((s == P - 1) ? 0 : s + 1);
     const double fl_prev = __shfl_sync(kFull, x[M], sprev);
     const double r = x[0] - c * fl_prev - b * x[1];
-    const double ys = schur_apply_lanes(C, r, s, P, gbase, sinvT);
+    const double ys = schur_apply_lanes<MODES>(C, r, s, P, gbase, sinvT);
     const double ys1 = __shfl_sync(kFull, ys, snext);
     x[0] = ys;
     const double cy = c * ys, by = b * ys1;
@@ -223,6 +242,7 @@ struct S1Args {
     const double* pstar;    // p^{n-1/2} + psi^{n-1/2}
     double* nadv[3];        // out: N(u^n)
     double* out[3];         // out: d1 (x-swept increment)
+    double* divn;           // out (if set): D.u^n at each cell, for the first psi pass (Step 3f)
     double dt, inv_rho, mu, invh, a1;   // a1 = 3/2, or 1 at n = 0
     int first, advection;
 };
@@ -403,6 +423,14 @@ __device__ __forceinline__ void s1_cell(const S1Args& A, int i, const RowB& rb, 
     s1_eval<DIM>(A, U, X, ps0, psm, Gv, d, Nv);
 #pragma unroll
     for (int c = 0; c < DIM; ++c) A.nadv[c][o[0]] = Nv[c];
+    if (A.divn) {
+        // D.u^n from operands already in registers: the first psi pass
+        // then reads one field instead of gathering u^n again for Step 3f's chi term
+        double dv = 0.0;
+#pragma unroll
+        for (int c = 0; c < DIM; ++c) dv += U[c][1 + 2 * c] - U[c][0];
+        A.divn[o[0]] = dv * A.invh;
+    }
 }
 
 // -------------------------------------------------------------------------------
@@ -417,6 +445,7 @@ struct LArgs {
     double* io[3];          // MID/USER: in-place data; LAST: increments in, u^{n+1} out; DIVPSI: psi out
     const double* un[3];    // LAST, DIVPSI: u^n
     const double* unew[3];  // DIVPSI: u^{n+1}
+    const double* divn;     // DIVPSI: D.u^n written by S1 (else gathered from u^n)
     double* p;              // DIVPSI: p -> q ; PSI_LAST: q -> p^{n+1/2}
     double* pstar;          // PSI_LAST: psi in, p* out
     double neg_rho_dt, chimu_half, invh;
@@ -539,14 +568,24 @@ struct LinePass {
                 ijk[0] = g0 + l;
                 if (AX == 1) { ijk[1] = m; ijk[2] = (int)tb; } else { ijk[1] = (int)tb; ijk[2] = m; }
                 double dn = 0.0, dol = 0.0;
+                if (A.divn) {
 #pragma unroll
-                for (int c = 0; c < DIM; ++c) {
-                    const unsigned qp = (ijk[c] == n - 1) ? q - (N - 1) * stp[c] : q + stp[c];
-                    dn += ldg(A.unew[c] + qp) - ldg(A.unew[c] + q);
-                    dol += ldg(A.un[c] + qp) - ldg(A.un[c] + q);
+                    for (int c = 0; c < DIM; ++c) {
+                        const unsigned qp = (ijk[c] == n - 1) ? q - (N - 1) * stp[c] : q + stp[c];
+                        dn += ldg(A.unew[c] + qp) - ldg(A.unew[c] + q);
+                    }
+                    dn *= A.invh;
+                    dol = ldg(A.divn + q);
+                } else {
+#pragma unroll
+                    for (int c = 0; c < DIM; ++c) {
+                        const unsigned qp = (ijk[c] == n - 1) ? q - (N - 1) * stp[c] : q + stp[c];
+                        dn += ldg(A.unew[c] + qp) - ldg(A.unew[c] + q);
+                        dol += ldg(A.un[c] + qp) - ldg(A.un[c] + q);
+                    }
+                    dn *= A.invh;
+                    dol *= A.invh;
                 }
-                dn *= A.invh;
-                dol *= A.invh;
                 tile[tile_off<L>(l, m, TP)] = A.neg_rho_dt * dn;         // Step 3e RHS
                 A.p[q] = A.p[q] - A.chimu_half * (dn + dol);             // Step 3f, explicit part
             });
@@ -585,7 +624,7 @@ struct LinePass {
             for (int l = w; l < R; l += nw)
 #pragma unroll 1
                 for (int c = 0; c < NC; ++c)
-                    ws_solve_smem<L>(tile + c * RTP + l * TP + lane * (L + 1), C, lane, P, 0, sinvT);
+                    ws_solve_smem<L, schur_modes(KIND)>(tile + c * RTP + l * TP + lane * (L + 1), C, lane, P, 0, sinvT);
             return;
         }
         const int lpw = (P <= 32) ? 32 / P : 1;          // lines per warp per round
@@ -602,7 +641,7 @@ struct LinePass {
                 double x[L];
 #pragma unroll
                 for (int i = 0; i < L; ++i) x[i] = tl[i];
-                ws_solve<L>(x, C, s, P, gbase, sinvT);
+                ws_solve<L, schur_modes(KIND)>(x, C, s, P, gbase, sinvT);
                 if (ok) {
 #pragma unroll
                     for (int i = 0; i < L; ++i) tl[i] = x[i];
@@ -642,10 +681,11 @@ struct LinePass {
     }
 };
 
-// (not needed when the line's S^{-1} is applied in banded form)
+// (not needed when the pass applies the line's S^{-1} in banded or circulant form)
+template <int MODES>
 __device__ __forceinline__ void load_sinvT(double* sinvT, const SchurInv* SI, const LineCoef& C)
 {
-    if (C.band >= 0) return;
+    if (((MODES & kSchurBand) && C.band >= 0) || ((MODES & kSchurCirc) && C.circ)) return;
     const int P = C.P;
     for (int e = threadIdx.x; e < P * P; e += blockDim.x) sinvT[e] = SI->sinvT[e];
 }
@@ -662,7 +702,7 @@ __global__ void __launch_bounds__(256, MINB) k_lines(const LineCoef C, const Sch
     double* sinvT = smem;
     double* tile = smem + P * P;
     double* tile2 = tile + (size_t)NC * R * TP;   // LAST: u^n, PSI_LAST: q (prefetched with the fill)
-    load_sinvT(sinvT, SI, C);                     // line factors: not written by the predecessor
+    load_sinvT<schur_modes(KIND)>(sinvT, SI, C);                     // line factors: not written by the predecessor
     pdl_wait();
     pdl_trigger();
     const int comp = (NC == 1) ? blockIdx.z : 0;
@@ -697,7 +737,7 @@ __global__ void __launch_bounds__(32 * WPB, MINB) k_xwarp(const LineCoef C, cons
     double* sinvT = smem;
     double* tile = smem + P * P + (size_t)w * NT * NC * lpw * TP;
     double* tile2 = tile + (size_t)NC * lpw * TP;
-    load_sinvT(sinvT, SI, C);
+    load_sinvT<schur_modes(KIND)>(sinvT, SI, C);
     __syncthreads();
     const int g0 = (blockIdx.x * WPB + w) * lpw;
     const int nrow = (DIM == 2) ? A.nl : n;
@@ -733,7 +773,7 @@ __global__ void __launch_bounds__(512) k_strided(const LineCoef C, const SchurIn
     double* yb = rr + P * RI;            // [P][RI] y_s
     double* ds = yb + P * RI;            // [P][RI] line sums of d (mean correction)
     double* xs = ds + P * RI;            // [P][RI] line sums of x
-    load_sinvT(sinvT, SI, C);
+    load_sinvT<schur_modes(KIND)>(sinvT, SI, C);
     const int il = threadIdx.x % RI, s = threadIdx.x / RI;
     const int i = blockIdx.x * RI + il;
     const int comp = (KIND == K_DIVPSI) ? 0 : blockIdx.z;
@@ -796,7 +836,8 @@ __global__ void __launch_bounds__(512) k_strided(const LineCoef C, const SchurIn
     rr[s * RI + il] = x[0] - c * xl[sp * RI + il] - b * x[1];
     __syncthreads();
     double ys = 0.0;
-    if (C.band >= 0) {
+    constexpr int MODES = schur_modes(KIND);
+    if ((MODES & kSchurBand) && C.band >= 0) {
         // banded circulant S^{-1} (LineCoef::band)
         ys = C.w[kMaxBand] * rr[s * RI + il];
 #pragma unroll
@@ -805,6 +846,13 @@ __global__ void __launch_bounds__(512) k_strided(const LineCoef C, const SchurIn
             const int qp = (s + d >= P) ? s + d - P : s + d, qm = (s - d < 0) ? s - d + P : s - d;
             ys = fma(C.w[kMaxBand + d], rr[qp * RI + il], ys);
             ys = fma(C.w[kMaxBand - d], rr[qm * RI + il], ys);
+        }
+    } else if ((MODES & kSchurCirc) && C.circ) {
+#pragma unroll
+        for (int d = 0; d < kMaxSeg; ++d) {
+            if (d >= P) break;
+            const int q = (s + d >= P) ? s + d - P : s + d;
+            ys = fma(C.wf[d], rr[q * RI + il], ys);
         }
     } else {
         for (int q = 0; q < P; ++q) ys = fma(sinvT[q * P + s], rr[q * RI + il], ys);
@@ -957,7 +1005,12 @@ static cudaError_t go_lines(Ctx* s, int sys, const LArgs& a, int ncomp_grid)
             // 256 threads per block: RI = 256 / P lines (measured: config 3 RI 16 0.1777 vs
             // 32 0.1818 ms/step; config 4 z sweep RI 8 771 vs 16 882 us); 512 for L = 32
             // (config 2 y sweep: RI 16 13.0 us, 8 14.8, 4 20.4; tiled 25.0)
-            const int RI = ri_env > 0 ? ri_env : std::max(8, std::min(32, (L > 16 ? 512 : 256) / s->P));
+            // round 2, banded S^{-1} (no staged S^{-1} left in shared memory): the z sweep
+            // at P = 32 takes 512 threads, RI 16 (config 4: 750 -> 686 us; y passes 424 ->
+            // 431, psi_y 232 -> 243 at RI 16, so they keep RI 8)
+            const bool wide = (KIND == K_LAST && AX == 2 && s->P >= 32);
+            const int RI = ri_env > 0 ? ri_env
+                                      : std::max(8, std::min(32, (L > 16 || wide ? 512 : 256) / s->P));
             if (s->n % RI == 0 && s->P * RI <= 512) {
                 auto kern = k_strided<L, KIND, DIM, AX>;
                 const size_t sm = ((size_t)s->P * s->P + 5 * (size_t)s->P * RI) * sizeof(double);
@@ -1070,6 +1123,21 @@ static cudaError_t go_axis(Ctx* s, int sys, int axis, const LArgs& a, int ncomp)
     IBGM_DISPATCH_L2D(s->L, (go_lines<LL, KIND, 2, 1, 1>(s, sys, a, ncomp)))
 }
 
+// S1 hands D.u^n to the first psi pass through the scratch field (single GPU: the slab
+// path's divergence kernels gather u^n themselves).  Measured (graph ms/step, same box):
+// config 4 4.361 -> 4.275 (div+psi_z 1058 -> 935 us, S1 1312 -> 1373 us); config 3
+// 0.1563 -> 0.1578, so 3D grids of N >= 256 only.  A/B switch: IBGM_DIVN=0 / 1 (force).
+static bool divn_fused(const Ctx* s)
+{
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("IBGM_DIVN");
+        v = e ? atoi(e) : 2;
+    }
+    if (v == 0 || !s->wrap || s->tmp == nullptr) return false;
+    return v == 1 || (s->dim == 3 && s->n >= 256);
+}
+
 cudaError_t launch_s1_x(Ctx* s, int first_step)
 {
     LArgs a{};
@@ -1081,6 +1149,7 @@ cudaError_t launch_s1_x(Ctx* s, int first_step)
     b.dt = s->dt; b.inv_rho = 1.0 / s->rho; b.mu = s->mu; b.invh = 1.0 / s->h;
     b.a1 = first_step ? 1.0 : 1.5;
     b.first = first_step; b.advection = s->advection;
+    b.divn = divn_fused(s) ? s->tmp : nullptr;
     if (s->dim == 3) { IBGM_DISPATCH_L(s->L, (go_lines<LL, K_S1, 3, 0, 3>(s, SYS_VISC, a, 1))) }
     IBGM_DISPATCH_L2D(s->L, (go_lines<LL, K_S1, 2, 0, 2>(s, SYS_VISC, a, 1)))
 }
@@ -1105,6 +1174,7 @@ cudaError_t launch_div_psi_first(Ctx* s, int axis)
     a.io[0] = a.io[1] = a.io[2] = s->pstar;
     for (int c = 0; c < 3; ++c) { a.un[c] = s->u[c]; a.unew[c] = s->st[c]; }
     a.p = s->p;
+    a.divn = divn_fused(s) ? s->tmp : nullptr;
     a.neg_rho_dt = -s->rho / s->dt;
     a.chimu_half = 0.5 * s->chi * s->mu;
     a.invh = 1.0 / s->h;

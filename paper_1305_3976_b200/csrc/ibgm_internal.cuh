@@ -40,6 +40,11 @@ struct LineCoef {
     // dense product; band = -1: dense S^{-1} (SchurInv).
     int band;
     double w[2 * kMaxBand + 1];
+    // circ = 1: S^{-1} is circulant, row 0 in wf (y_s = sum_d wf[d] r_{(s+d) mod P}, the
+    // coefficients uniform across lanes: constant-bank operands instead of a staged
+    // P x P matrix); 0: dense S^{-1} (SchurInv)
+    int circ;
+    double wf[kMaxSeg];
 };
 
 // dense inverse of the P x P periodic Schur matrix S and its column sums (device)
