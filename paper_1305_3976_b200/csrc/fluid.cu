@@ -318,6 +318,9 @@ __device__ __forceinline__ RowB row_bases(int j, int k, int n, int nl, int wrap)
 #ifndef IBGM_PF_DIV
 #define IBGM_PF_DIV 1           // prefetch in the divergence fill of the first psi pass (N <= 128)
 #endif
+#ifndef IBGM_DIV_CHUNK
+#define IBGM_DIV_CHUNK 1        // contiguous-chunk, two-cells-in-flight fill when S1 supplies D.u^n
+#endif
 __device__ __forceinline__ void pf_l2(const double* p)
 {
     if (IBGM_PF_L1) asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
@@ -548,8 +551,84 @@ struct LinePass {
                         for (int c = 0; c < NC; ++c) tile[c * RTP + off] = v[c];
                     }
             }
+        } else if (KIND == K_DIVPSI && AX != 0 && IBGM_DIV_CHUNK) {
+            if (A.divn) {
+                div_fill_chunk(tile, A, n, R, TP, g0, tb, t, T);
+                return;
+            }
+            div_fill_gather(tile, A, n, nrow, R, TP, g0, tb, t, T);
         } else if (KIND == K_DIVPSI) {
-            // D.u at each cell for u^{n+1} and u^n
+            div_fill_gather(tile, A, n, nrow, R, TP, g0, tb, t, T);
+        } else {
+            // pure copies: cp.async keeps every load of the tile in flight at once
+            issue(tile, tile2, A, n, R, TP, g0, tb, comp, t, T);
+            cp_async_wait_all();
+        }
+    }
+
+    // The first psi pass's fill with D.u^n from S1 (A.divn): each thread walks a contiguous
+    // chunk of its line, so u^{n+1}_AX(I + e_AX) of one cell is u^{n+1}_AX(I) of the next,
+    // and the operands of cell m+1 are loaded before cell m is evaluated and p stored
+    // (two cells in flight per thread: the fill was bound by one load latency per cell).
+    static __device__ __forceinline__ void div_fill_chunk(double* tile, const LArgs& A, int n, int R, int TP, int g0,
+                                                          unsigned tb, int t, int T)
+    {
+        const unsigned N = (unsigned)n;
+        const unsigned stp[3] = {1u, N, N * N};
+        const int lg = 31 - __clz(R);
+        const int l = t & (R - 1);
+        if (g0 + l >= n) return;
+        const int nthr = T >> lg;                       // threads per line
+        const int chunk = (n + nthr - 1) / nthr;
+        const int mb = (t >> lg) * chunk, me = min(n, mb + chunk);
+        if (mb >= me) return;
+        const unsigned S = stp[AX];
+        const unsigned base = (unsigned)(g0 + l) + ((AX == 1) ? N * N * tb : N * tb);
+        int ijk[3];
+        ijk[0] = g0 + l;
+        ijk[1] = (AX == 1) ? 0 : (int)tb;
+        ijk[2] = (AX == 2) ? 0 : (int)tb;
+        // operands of one cell: u_c^{n+1}(I + e_c), u_c^{n+1}(I) for c != AX, u_AX^{n+1}(I + e_AX),
+        // D.u^n, p
+        struct Ops {
+            double up[3], u0[3], dv, pp;
+        };
+        auto load = [&](int m, Ops& o) {
+            const unsigned q = base + S * (unsigned)m;
+#pragma unroll
+            for (int c = 0; c < DIM; ++c) {
+                const int ic = (c == AX) ? m : ijk[c];
+                const unsigned qp = (ic == n - 1) ? q - (N - 1) * stp[c] : q + stp[c];
+                o.up[c] = ldg(A.unew[c] + qp);
+                o.u0[c] = (c == AX) ? 0.0 : ldg(A.unew[c] + q);
+            }
+            o.dv = ldg(A.divn + q);
+            o.pp = A.p[q];
+        };
+        double zc = ldg(A.unew[AX] + base + S * (unsigned)mb);
+        Ops cur, nxt;
+        load(mb, cur);
+        for (int m = mb; m < me; ++m) {
+            if (m + 1 < me) load(m + 1, nxt);
+            double dn = cur.up[AX] - zc;
+#pragma unroll
+            for (int c = 0; c < DIM; ++c)
+                if (c != AX) dn += cur.up[c] - cur.u0[c];
+            dn *= A.invh;
+            const unsigned q = base + S * (unsigned)m;
+            tile[tile_off<L>(l, m, TP)] = A.neg_rho_dt * dn;               // Step 3e RHS
+            A.p[q] = cur.pp - A.chimu_half * (dn + cur.dv);                 // Step 3f, explicit part
+            zc = cur.up[AX];
+            cur = nxt;
+        }
+    }
+
+    // The first psi pass's fill, D.u^{n+1} and D.u^n gathered at every cell
+    static __device__ __forceinline__ void div_fill_gather(double* tile, const LArgs& A, int n, int nrow, int R,
+                                                           int TP, int g0, unsigned tb, int t, int T)
+    {
+        const unsigned N = (unsigned)n;
+        {
             const unsigned stp[3] = {1u, N, N * N};
             const int mstep = (AX == 0) ? 0 : (T >> (31 - __clz(R)));   // this thread's next position
             for_tile<AX>(n, nrow, R, g0, tb, t, T, [&](int l, int m, unsigned q) {
@@ -589,10 +668,6 @@ struct LinePass {
                 tile[tile_off<L>(l, m, TP)] = A.neg_rho_dt * dn;         // Step 3e RHS
                 A.p[q] = A.p[q] - A.chimu_half * (dn + dol);             // Step 3f, explicit part
             });
-        } else {
-            // pure copies: cp.async keeps every load of the tile in flight at once
-            issue(tile, tile2, A, n, R, TP, g0, tb, comp, t, T);
-            cp_async_wait_all();
         }
     }
 
