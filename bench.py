@@ -47,11 +47,11 @@ ALG_DOUBLES = {
 
 
 def alg_doubles(dim, n, world=1):
-    """Per-phase doubles per cell for this grid: on one GPU, 3D grids of N >= 256 hand
-    D.u^n from S1 to the first psi pass (S1 writes one more field, the psi pass reads it
-    instead of the three u^n components)."""
+    """Per-phase doubles per cell for this grid: 3D grids of N >= 256 hand D.u^n from S1
+    to the first psi pass (S1 writes one more field, the psi pass reads it instead of the
+    three u^n components), on one GPU and on z-slabs alike."""
     a = dict(ALG_DOUBLES[dim])
-    if dim == 3 and n >= 256 and world == 1:
+    if dim == 3 and n >= 256:
         a["s1_rhs_xsweep"], a["div_psi_first"] = 14, 7
     return a
 

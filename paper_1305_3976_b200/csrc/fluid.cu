@@ -495,7 +495,6 @@ struct LinePass {
     static __device__ __forceinline__ void fill(double* tile, double* tile2, const LArgs& A, int n, int R, int TP,
                                                 int g0, unsigned tb, int comp, int t, int T)
     {
-        const unsigned N = (unsigned)n;
         const unsigned RTP = (unsigned)R * TP;
         const int nrow = (DIM == 2) ? A.nl : n;
         if (KIND == K_S1) {
@@ -1198,18 +1197,18 @@ static cudaError_t go_axis(Ctx* s, int sys, int axis, const LArgs& a, int ncomp)
     IBGM_DISPATCH_L2D(s->L, (go_lines<LL, KIND, 2, 1, 1>(s, sys, a, ncomp)))
 }
 
-// S1 hands D.u^n to the first psi pass through the scratch field (single GPU: the slab
-// path's divergence kernels gather u^n themselves).  Measured (graph ms/step, same box):
-// config 4 4.361 -> 4.275 (div+psi_z 1058 -> 935 us, S1 1312 -> 1373 us); config 3
-// 0.1563 -> 0.1578, so 3D grids of N >= 256 only.  A/B switch: IBGM_DIVN=0 / 1 (force).
-static bool divn_fused(const Ctx* s)
+// S1 hands D.u^n to the first psi pass through the scratch field (on a slab: to the
+// cut-axis forward phase, slab.cu).  Measured (graph ms/step, same box): config 4 4.361
+// -> 4.275 (div+psi_z 1058 -> 935 us, S1 1312 -> 1373 us); config 3 0.1563 -> 0.1578,
+// so 3D grids of N >= 256 only.  A/B switch: IBGM_DIVN=0 / 1 (force).
+bool divn_fused(const Ctx* s)
 {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("IBGM_DIVN");
         v = e ? atoi(e) : 2;
     }
-    if (v == 0 || !s->wrap || s->tmp == nullptr) return false;
+    if (v == 0 || s->tmp == nullptr) return false;
     return v == 1 || (s->dim == 3 && s->n >= 256);
 }
 

@@ -257,6 +257,7 @@ void make_line_coef(LineCoef* C, SchurInv* S, int64_t N, int L, double c, double
 
 // launchers (fluid.cu)
 cudaError_t launch_s1_x(Ctx* s, int first_step);             // Steps 3a-3c: p*, momentum, x sweep
+bool divn_fused(const Ctx* s);                               // S1 stores D.u^n for the first psi pass
 cudaError_t launch_sweep_mid(Ctx* s, int axis);              // Step 3d: a middle Douglas sweep
 cudaError_t launch_sweep_last(Ctx* s, int axis);             // last Douglas sweep, u^{n+1} = u^n + delta
 cudaError_t launch_div_psi_first(Ctx* s, int axis);          // Step 3e RHS + first psi factor + q (3f)

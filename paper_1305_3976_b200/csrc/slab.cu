@@ -133,6 +133,7 @@ struct SlabArgs {
     const double* un[3];      // u^n (EPI_ADD_UN; SRC_DIV)
     const double* unew[3];    // u^{n+1} (SRC_DIV)
     double* p;                // SRC_DIV: p -> q = p - chi mu D.(u^{n+1}+u^n)/2
+    const double* divn;       // SRC_DIV: D.u^n written by S1 (else gathered from u^n)
     // reduced-system exchange with a master rank per line (m = line mod P)
     double* up_w;             // writer: this rank's block for master 0; + m * up_mstride for master m
     long long up_mstride;
@@ -186,10 +187,10 @@ __global__ void __launch_bounds__(128) k_slab_fwd(SlabCf C, SlabArgs A, int slot
         for (int c = 0; c < DIM; ++c) {
             const long long o = (c == DIM - 1) ? PL : off[c];
             dn += A.unew[c][fg + o] - A.unew[c][fg];
-            dol += A.un[c][fg + o] - A.un[c][fg];
+            if (!A.divn) dol += A.un[c][fg + o] - A.un[c][fg];
         }
         dn *= A.invh;
-        dol *= A.invh;
+        dol = A.divn ? A.divn[fg] : dol * A.invh;
         A.p[fg] = A.p[fg] - A.chimu_half * (dn + dol);
         const double r = A.neg_rho_dt * dn;
         io[f] = r;
@@ -253,6 +254,9 @@ __global__ void __launch_bounds__(128) k_slab_fwd_reg(SlabCf C, SlabArgs A, int 
             off[1] = PL;
         }
     }
+    // (the updated p of each plane is kept and stored after the loads of the whole column:
+    //  a store between them would keep the next plane's loads from being issued early)
+    double pq[(SRC == SRC_DIV) ? MAXM + 1 : 1];
     auto src = [&](int kl) -> double {
         const long long f = kl * PL + q;
         if (SRC == SRC_FIELD) return io[f];
@@ -261,12 +265,12 @@ __global__ void __launch_bounds__(128) k_slab_fwd_reg(SlabCf C, SlabArgs A, int 
 #pragma unroll
         for (int c = 0; c < DIM; ++c) {
             const long long o = (c == DIM - 1) ? PL : off[c];
-            dn += A.unew[c][fg + o] - A.unew[c][fg];
-            dol += A.un[c][fg + o] - A.un[c][fg];
+            dn += __ldg(A.unew[c] + fg + o) - __ldg(A.unew[c] + fg);
+            if (!A.divn) dol += __ldg(A.un[c] + fg + o) - __ldg(A.un[c] + fg);
         }
         dn *= A.invh;
-        dol *= A.invh;
-        A.p[fg] = A.p[fg] - A.chimu_half * (dn + dol);
+        dol = A.divn ? __ldg(A.divn + fg) : dol * A.invh;
+        pq[(SRC == SRC_DIV) ? kl : 0] = A.p[fg] - A.chimu_half * (dn + dol);
         return A.neg_rho_dt * dn;
     };
     const double c = C.c(), b = C.b();
@@ -276,6 +280,11 @@ __global__ void __launch_bounds__(128) k_slab_fwd_reg(SlabCf C, SlabArgs A, int 
     double d[MAXM + 1];
 #pragma unroll
     for (int i = 0; i <= MAXM; ++i) d[i] = (i <= m) ? src(i) : 0.0;
+    if (SRC == SRC_DIV) {
+#pragma unroll
+        for (int i = 0; i <= MAXM; ++i)
+            if (i <= m) A.p[(long long)(k0 + i) * PL + q] = pq[i];
+    }
     double dsum = 0.0;
 #pragma unroll
     for (int i = 0; i <= MAXM; ++i) dsum += d[i];
@@ -511,6 +520,7 @@ cudaError_t slab_divpsi_fwd(Ctx* s, Group* G)
     a.io[0] = a.io[1] = a.io[2] = s->pstar;
     for (int c = 0; c < s->dim; ++c) { a.un[c] = s->u[c]; a.unew[c] = s->st[c]; }
     a.p = s->p;
+    a.divn = divn_fused(s) ? s->tmp : nullptr;
     SlabCf C{G->coef[SYS_PSI], (int)(s->nl / G->Q) - 1, G->P * G->Q};
     if (s->dim == 3) return launch_fwd<3, SRC_DIV, 1>(s, C, a, 1);
     return launch_fwd<2, SRC_DIV, 1>(s, C, a, 1);

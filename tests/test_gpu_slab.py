@@ -228,3 +228,40 @@ def test_config4_full_size_eight_slabs_matches_single_gpu():
     for c in range(3):
         assert _rel(fg["u"][c], f1["u"][c]) <= 1e-10, c
     assert _rel(fg["p"], f1["p"]) <= 1e-10 and _rel(fg["X"], f1["X"]) <= 1e-10
+
+
+_DIVN_CASE = r"""
+import sys
+import numpy as np
+sys.path.insert(0, {root!r})
+from paper_1305_3976_b200 import ibgm, inputs
+from oracle import oracle as O
+pr = inputs.config(4, n=96, nodes=4000)
+o = O.Oracle(pr.dim, pr.n, pr.mu, pr.rho, pr.dt, chi=pr.chi, kernel=pr.kernel, H=pr.H)
+o.set_fields(*pr.u, p=pr.p)
+o.set_boundary(pr.X, pr.edges, pr.kappa, rest=pr.rest, weight=pr.weight)
+o.step(10)
+fo = o.fields()
+rel = lambda a, b: float(np.abs(a - b).max() / np.abs(b).max())
+for P in (1, 4):
+    g = ibgm.from_problem(pr) if P == 1 else ibgm.from_problem(pr, nranks=P, transport=1)
+    g.step(10)
+    fg = g.fields()
+    g.close()
+    errs = [rel(fg["u"][c], fo["u"][c]) for c in range(3)] + [rel(fg["p"], fo["p"]), rel(fg["X"], fo["X"])]
+    print(P, errs)
+    assert max(errs) <= 1e-9, (P, errs)
+"""
+
+
+def test_divn_handoff_forced_on_a_small_grid():
+    """S1 hands D.u^n to the first psi pass (single GPU: k_lines fill; slabs: the cut-axis
+    forward phase) only at N >= 256 by default; IBGM_DIVN=1 forces it on config 4 at
+    N = 96 in a fresh process: 10 steps vs the oracle on one GPU and on 4 slabs."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _DIVN_CASE.format(root=root)], capture_output=True, text=True,
+                       env=dict(os.environ, IBGM_DIVN="1"), timeout=900)
+    assert r.returncode == 0, r.stdout + r.stderr
