@@ -342,6 +342,21 @@ static int upload_coef(Ctx* s, int sys, double c, double a, double b, int mf)
     CKC(cudaMalloc(&G->coef[sys], v.size() * sizeof(double)));
     CKC(cudaMemcpyAsync(G->coef[sys], v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice, s->stream));
     CKC(cudaStreamSynchronize(s->stream));
+    if (sys == SYS_VISC) {
+        // is the cut-axis S^{-1} diagonal to rounding?  (A/B switch: IBGM_SLAB_LOCAL=0)
+        const int PQ = G->P * G->Q, m = (int)(s->n / PQ) - 1;
+        const double* S = v.data() + SC_HDR + 4 * m;
+        const double ref = std::fabs(S[0]);
+        bool diag = PQ > 1 && ref > 0;
+        for (int p = 0; p < PQ && diag; ++p)
+            for (int q = 0; q < PQ; ++q) {
+                const double e = std::fabs(S[p * PQ + q]);
+                if ((p == q) ? std::fabs(e - ref) > 1e-14 * ref : e > 1e-18 * ref) { diag = false; break; }
+            }
+        const char* el = getenv("IBGM_SLAB_LOCAL");
+        G->visc_local = (diag && !(el && atoi(el) == 0)) ? 1 : 0;
+        G->visc_w0 = S[0];
+    }
     return IB_OK;
 }
 
@@ -1148,9 +1163,14 @@ static int enqueue_step_slab(Ctx* s, int first)
     // the last Douglas sweep along the cut axis (distributed Schur solve)
     if (s->profiling) CKC(cudaEventRecord(s->ev[last_ph][0], s->stream));
     FOR_SLABS(slab_sweep_last_fwd(sl, G));
-    CKG(group_up(G, 2 * d, s->stream));
-    CKC(slab_master(G->slab[0], G, SYS_VISC, d, 2 * d, 0));
-    CKG(group_dn(G, d, s->stream));
+    if (G->visc_local) {
+        // S^{-1} diagonal: each part's y from its neighbour parts (nearest-neighbour exchange)
+        CKG(group_edge(G, d, s->stream));
+    } else {
+        CKG(group_up(G, 2 * d, s->stream));
+        CKC(slab_master(G->slab[0], G, SYS_VISC, d, 2 * d, 0));
+        CKG(group_dn(G, d, s->stream));
+    }
     FOR_SLABS(slab_sweep_last_corr(sl, G));
     if (s->profiling) {
         CKC(cudaEventRecord(s->ev[last_ph][1], s->stream));

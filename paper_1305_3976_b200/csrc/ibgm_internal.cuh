@@ -170,6 +170,11 @@ struct Group {
     void* comm;                       // ncclComm_t
     void* comm_side;                  // a second communicator (ncclCommSplit) for the IB
                                       // look-ahead's all-reduce on the side stream
+    // the viscous cut-axis system's S^{-1} is diagonal to rounding (every off-diagonal
+    // entry below 1e-18 of the diagonal): y_t = w0 r_t, so each part needs only its
+    // neighbour parts' scalars -- a nearest-neighbour exchange instead of the line masters
+    int visc_local;
+    double visc_w0;
 };
 
 struct HaloSpec {
@@ -196,6 +201,7 @@ cudaError_t slab_spread_part(Ctx* top, Ctx* s, int* list, int* count);
 int group_halo(Group* G, int nf, const HaloSpec* spec, cudaStream_t st);
 int group_up(Group* G, int ns, cudaStream_t st);          // scalars to the line masters
 int group_dn(Group* G, int ncomp, cudaStream_t st);       // y and corrections back
+int group_edge(Group* G, int ncomp, cudaStream_t st);     // neighbour parts' scalars (visc_local)
 cudaError_t slab_master(Ctx* s, Group* G, int sys, int ncomp, int ns, int mf);
 int group_allreduce_U(Group* G, Ctx* top, cudaStream_t st, bool side = false);
 int nccl_comm_split(void* comm, int rank, void** out);      // ncclCommSplit (0 ok; -1 unavailable)

@@ -149,6 +149,12 @@ struct SlabArgs {
     int Q, Lseg;              // Schur parts per slab and their length (nz = Q Lseg)
     int ns;                   // gather slots per part of this solve (6 viscous: 2 per component; 4 psi)
     long long plane;          // N^{d-1}
+    // visc_local (S^{-1} diagonal): this slab's scalars A_t, fm_t in edge_w [comp][Q][2][plane],
+    // the neighbours' in edge_r [2][comp][plane] (fm of the part below, A of the part above)
+    int local;
+    double w0;
+    double* edge_w;
+    const double* edge_r;
 };
 
 // forward phase: interior Thomas solve of every line of this slab, in place (plane 0
@@ -214,6 +220,12 @@ __global__ void __launch_bounds__(128) k_slab_fwd(SlabCf C, SlabArgs A, int slot
         x = io[i * PL + q] - cpv[i - 1] * x;
         io[i * PL + q] = x;
         fsum += x;
+    }
+    if (A.local) {                      // A_t and fm_t of this part (visc_local)
+        double* e = A.edge_w + ((long long)(comp * A.Q + blockIdx.z) * 2) * PL + q;
+        e[0] = d0 - b * x;
+        e[PL] = fm;
+        return;
     }
     // to the line's master: [sub][slot][idx] in the block for master m
     {
@@ -310,6 +322,12 @@ __global__ void __launch_bounds__(128) k_slab_fwd_reg(SlabCf C, SlabArgs A, int 
             io[i * PL + q] = d[i];
             fsum += d[i];
         }
+    if (A.local) {                      // A_t and fm_t of this part (visc_local)
+        double* e = A.edge_w + ((long long)(comp * A.Q + blockIdx.z) * 2) * PL + q;
+        e[0] = d[0] - b * d[1];
+        e[PL] = fm;
+        return;
+    }
     {
         const int P = C.P / A.Q, mst = (int)(q % P);
         const long long idx = q / P;
@@ -339,13 +357,27 @@ __global__ void __launch_bounds__(128) k_slab_corr(SlabCf C, SlabArgs A, int slo
     const long long PL = A.plane;
     const int P = C.P / A.Q;
     const double c = C.c(), b = C.b();
-    // y_s, y_{s+1} and the line-mean correction from the line's master
-    const int mst = (int)(q % P);
-    const long long idx = q / P;
-    const double* y = A.dn_r + ((long long)mst * 3 + comp) * A.nb * A.nidx + idx;
     const int sub = part - A.rank * A.Q;
-    const double ys = y[(long long)sub * A.nidx], ys1 = y[(long long)(sub + 1) * A.nidx];
-    const double corr = MF ? y[(long long)(A.Q + 1) * A.nidx] : 0.0;
+    double ys, ys1, corr = 0.0;
+    if (A.local) {
+        // visc_local: y_t = w0 (A_t - c fm_{t-1}), y_{t+1} = w0 (A_{t+1} - c fm_t), the
+        // neighbour parts of the slab's first / last part from the exchanged planes
+        const double* e = A.edge_w + (long long)comp * A.Q * 2 * PL + q;
+        const double At = e[(long long)(2 * sub) * PL], fmt = e[(long long)(2 * sub + 1) * PL];
+        const double fmp = (sub > 0) ? e[(long long)(2 * sub - 1) * PL] : A.edge_r[(long long)comp * PL + q];
+        const double An = (sub < A.Q - 1) ? e[(long long)(2 * sub + 2) * PL]
+                                          : A.edge_r[(long long)(3 + comp) * PL + q];
+        ys = A.w0 * (At - c * fmp);
+        ys1 = A.w0 * (An - c * fmt);
+    } else {
+        // y_s, y_{s+1} and the line-mean correction from the line's master
+        const int mst = (int)(q % P);
+        const long long idx = q / P;
+        const double* y = A.dn_r + ((long long)mst * 3 + comp) * A.nb * A.nidx + idx;
+        ys = y[(long long)sub * A.nidx];
+        ys1 = y[(long long)(sub + 1) * A.nidx];
+        corr = MF ? y[(long long)(A.Q + 1) * A.nidx] : 0.0;
+    }
     (void)slot0;
     const double* g = C.g();
     const double* h = C.h();
@@ -477,6 +509,8 @@ static SlabArgs slab_args(Ctx* s, Group* G, int ns)
     a.dn_wmstride = emu ? ds : 0;
     a.dn_rstride = blk2;
     a.dn_r = G->dn_rv + me * ds;
+    a.edge_w = a.up_w;                                    // visc_local layouts (set by the sweeps)
+    a.edge_r = G->up_rv + me * us;
     return a;
 }
 
@@ -497,6 +531,8 @@ cudaError_t slab_master(Ctx* s, Group* G, int sys, int ncomp, int ns, int mf)
 cudaError_t slab_sweep_last_fwd(Ctx* s, Group* G)
 {
     SlabArgs a = slab_args(s, G, 2 * s->dim);
+    a.local = G->visc_local;
+    a.w0 = G->visc_w0;
     for (int c = 0; c < s->dim; ++c) { a.io[c] = s->st[c]; a.un[c] = s->u[c]; }
     SlabCf C{G->coef[SYS_VISC], (int)(s->nl / G->Q) - 1, G->P * G->Q};
     if (s->dim == 3) return launch_fwd<3, SRC_FIELD, 0>(s, C, a, 3);
@@ -506,6 +542,8 @@ cudaError_t slab_sweep_last_fwd(Ctx* s, Group* G)
 cudaError_t slab_sweep_last_corr(Ctx* s, Group* G)
 {
     SlabArgs a = slab_args(s, G, 2 * s->dim);
+    a.local = G->visc_local;
+    a.w0 = G->visc_w0;
     for (int c = 0; c < s->dim; ++c) { a.io[c] = s->st[c]; a.un[c] = s->u[c]; }
     SlabCf C{G->coef[SYS_VISC], (int)(s->nl / G->Q) - 1, G->P * G->Q};
     k_slab_corr<EPI_ADD_UN, 0><<<dim3(nb128(s->plane), (unsigned)s->dim, (unsigned)a.Q), 128, 0, s->stream>>>(C, a, 0);
@@ -976,6 +1014,43 @@ int group_dn(Group* G, int ncomp, cudaStream_t st)
     for (int r = 0; r < G->P; ++r) {
         NCK(g_nccl.Send(G->dn_s + r * stride, cnt, kNcclDouble, r, G->comm, st));
         NCK(g_nccl.Recv(G->dn_rv + r * stride, cnt, kNcclDouble, r, G->comm, st));
+    }
+    NCK(g_nccl.GroupEnd());
+    return 0;
+}
+
+// visc_local: the scalars of each slab's boundary parts to its neighbours (the
+// nearest-neighbour exchange of PAPER.md:807-833 applied to the reduced system): fm of
+// the last part -> the slab above (receive slot 0), A of the first part -> the slab
+// below (receive slot 1); one plane per component each way
+int group_edge(Group* G, int ncomp, cudaStream_t st)
+{
+    const int P = G->P, Q = G->Q;
+    const long long PL = G->slab[0]->plane;
+    const long long us = (long long)up_rank_size(G, PL);
+    if (G->transport == IB_TRANSPORT_EMULATE) {
+        HaloPtrs H{};
+        int np = 0;
+        for (int c = 0; c < ncomp; ++c)
+            for (int r = 0; r < P; ++r) {
+                const double* e = G->up_s + r * us + (long long)c * Q * 2 * PL;
+                H.src[np] = e + (long long)(2 * (Q - 1) + 1) * PL;                     // fm of the last part
+                H.dst[np++] = G->up_rv + ((r + 1) % P) * us + (long long)c * PL;      // -> above, slot 0
+                H.src[np] = e;                                                        // A of the first part
+                H.dst[np++] = G->up_rv + ((r + P - 1) % P) * us + (long long)(3 + c) * PL;   // -> below, slot 1
+            }
+        const long long bx = std::min((PL + 255) / 256, 32LL);
+        k_halo_copy<<<dim3((unsigned)bx, (unsigned)np), 256, 0, st>>>(H, PL);
+        return (int)cudaGetLastError();
+    }
+    const int up = (G->rank + 1) % P, dn = (G->rank + P - 1) % P;
+    NCK(g_nccl.GroupStart());
+    for (int c = 0; c < ncomp; ++c) {
+        const double* e = G->up_s + (long long)c * Q * 2 * PL;
+        NCK(g_nccl.Send(e + (long long)(2 * (Q - 1) + 1) * PL, (size_t)PL, kNcclDouble, up, G->comm, st));
+        NCK(g_nccl.Recv(G->up_rv + (long long)c * PL, (size_t)PL, kNcclDouble, dn, G->comm, st));
+        NCK(g_nccl.Send(e, (size_t)PL, kNcclDouble, dn, G->comm, st));
+        NCK(g_nccl.Recv(G->up_rv + (long long)(3 + c) * PL, (size_t)PL, kNcclDouble, up, G->comm, st));
     }
     NCK(g_nccl.GroupEnd());
     return 0;
