@@ -649,6 +649,7 @@ int ib_create(const ib_grid* grid, double nu, double rho, double dt, const ib_op
             if (nr != 0) return fail(IB_ENCCL, "ncclCommInitRank: %s", nccl_error_string(nr));
             // (collective; without ncclCommSplit the slab look-ahead stays off)
             if (nccl_comm_split(G->comm, o.rank, &G->comm_side) != 0) G->comm_side = nullptr;
+            if (nccl_comm_split(G->comm, o.rank, &G->comm_halo) != 0) G->comm_halo = nullptr;
         }
     }
     {
@@ -663,6 +664,11 @@ int ib_create(const ib_grid* grid, double nu, double rho, double dt, const ib_op
         CKC(cudaStreamCreateWithPriority(&s->side, cudaStreamNonBlocking, prio));
         CKC(cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming));
         CKC(cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming));
+        if (s->grp) {
+            CKC(cudaStreamCreateWithFlags(&s->comm, cudaStreamNonBlocking));
+            CKC(cudaEventCreateWithFlags(&s->ev_h0, cudaEventDisableTiming));
+            CKC(cudaEventCreateWithFlags(&s->ev_h1, cudaEventDisableTiming));
+        }
         const char* el = getenv("IBGM_LOOKAHEAD");
         s->lookahead = (el && atoi(el) == 0) ? 0 : 1;
     }
@@ -711,6 +717,7 @@ int ib_set_fields(ib_ctx* c, const double* u, const double* v, const double* w, 
     clear_errors(s);
     s->step = 0;
     s->fields_set = true;
+    s->u_halo_ready = false;
     return IB_OK;
 }
 
@@ -893,6 +900,7 @@ static cudaError_t clear3(Ctx* s, double* const* f)
 
 static int enqueue_step(Ctx* s, int first);
 static int enqueue_step_slab(Ctx* s, int first);
+static bool early_halo_on(const Ctx* s);
 
 static void swap_state(Ctx* s)
 {
@@ -989,7 +997,10 @@ int ib_step(ib_ctx* c, int64_t nsteps)
     }
     for (int64_t t = 0; t < nsteps; ++t) {
         const int first = (s->step == 0);
-        if (!first && !s->profiling && s->use_graphs && !s->debug_keep_f) {
+        // (on z-slabs a captured step expects the u halos from the step before: after
+        //  ib_set_fields / ib_set_state one step runs eagerly with the full exchange)
+        const bool halo_ok = !s->grp || s->u_halo_ready || !early_halo_on(s);
+        if (!first && !s->profiling && s->use_graphs && !s->debug_keep_f && halo_ok) {
             // replay the captured regular step for the current pointer parity and
             // look-ahead state
             const int par = s->parity * 2 + (s->ib_ahead ? 1 : 0);
@@ -1085,6 +1096,20 @@ static double* fld_u1(Ctx* c) { return c->u[1]; }
 static double* fld_u2(Ctx* c) { return c->u[2]; }
 static double* fld_pstar(Ctx* c) { return c->pstar; }
 static double* fld_st_last2(Ctx* c) { return c->st[1]; }
+static double* fld_st0(Ctx* c) { return c->st[0]; }
+static double* fld_st1(Ctx* c) { return c->st[1]; }
+
+// the early u halos (A/B switch: IBGM_EARLY_HALO=0); NCCL needs the third communicator
+static bool early_halo_on(const Ctx* s)
+{
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("IBGM_EARLY_HALO");
+        v = (e && atoi(e) == 0) ? 0 : 1;
+    }
+    const Group* G = s->grp;
+    return v == 1 && G && s->comm && (G->transport == IB_TRANSPORT_EMULATE || G->comm_halo != nullptr);
+}
 static double* fld_st_last3(Ctx* c) { return c->st[2]; }
 
 // The same step on a z-slab decomposition: each phase runs on every local slab, with
@@ -1140,11 +1165,13 @@ static int enqueue_step_slab(Ctx* s, int first)
         if (rc != IB_OK) return rc;
     }
     if (s->profiling) CKC(cudaEventRecord(s->ev[IB_PH_S1][0], s->stream));
-    // halos for Steps 3a-3b: u (every component) on both sides, p* below
+    // halos for Steps 3a-3b: u (every component) on both sides, p* below -- u's already
+    // arrived during the previous step's psi passes when u_halo_ready
     {
         HaloSpec h[4] = {{fld_u0, true, true}, {fld_u1, true, true}, {fld_u2, true, true}, {fld_pstar, true, false}};
         if (d == 2) h[2] = h[3];
-        CKG(group_halo(G, d + 1, h, s->stream));
+        if (s->u_halo_ready && early_halo_on(s)) CKG(group_halo(G, 1, h + d, s->stream));
+        else CKG(group_halo(G, d + 1, h, s->stream));
     }
     FOR_SLABS(launch_s1_x(sl, first));
     if (s->profiling) {
@@ -1207,6 +1234,17 @@ static int enqueue_step_slab(Ctx* s, int first)
         HaloSpec h[1] = {{d == 3 ? fld_st_last3 : fld_st_last2, false, true}};
         CKG(group_halo(G, 1, h, s->stream));
     }
+    // the rest of u^{n+1}'s halos for the next step's S1, on the comm stream while the psi
+    // passes run (u^{n+1} is final here; joined at the end of the step)
+    const bool early = early_halo_on(s);
+    if (early) {
+        HaloSpec h[3] = {{fld_st0, true, true}, {fld_st1, true, true}, {d == 3 ? fld_st_last3 : fld_st_last2, true, false}};
+        if (d == 2) h[1] = h[2];
+        CKC(cudaEventRecord(s->ev_h0, s->stream));
+        CKC(cudaStreamWaitEvent(s->comm, s->ev_h0, 0));
+        CKG(group_halo(G, d, h, s->comm, G->comm_halo));
+        CKC(cudaEventRecord(s->ev_h1, s->comm));
+    }
     FOR_SLABS(slab_divpsi_fwd(sl, G));
     CKG(group_up(G, 4, s->stream));
     CKC(slab_master(G->slab[0], G, SYS_PSI, 1, 4, 1));
@@ -1232,6 +1270,8 @@ static int enqueue_step_slab(Ctx* s, int first)
     }
     if (look) CKC(cudaStreamWaitEvent(s->stream, s->ev_join, 0));
     s->ib_ahead = look;
+    if (early) CKC(cudaStreamWaitEvent(s->stream, s->ev_h1, 0));
+    s->u_halo_ready = early;
     return IB_OK;
 }
 
@@ -1438,6 +1478,7 @@ int ib_set_state(ib_ctx* c, const void* buf, int64_t bytes)
     s->step = h.step;
     s->ib_ahead = h.ib_ahead != 0;
     s->fields_set = true;
+    s->u_halo_ready = false;
     return IB_OK;
 }
 
@@ -1601,6 +1642,7 @@ int ib_destroy(ib_ctx* c)
         for (int k = 0; k < SYS_COUNT; ++k) cudaFree(G->coef[k]);
         free_lagrangian(s);
         nccl_comm_destroy(G->comm_side);
+        nccl_comm_destroy(G->comm_halo);
         nccl_comm_destroy(G->comm);
         delete G;
         s->grp = nullptr;
@@ -1616,6 +1658,9 @@ int ib_destroy(ib_ctx* c)
     if (s->ev_made)
         for (int ph = 0; ph < IB_NPHASES; ++ph) { cudaEventDestroy(s->ev[ph][0]); cudaEventDestroy(s->ev[ph][1]); }
     if (s->side) cudaStreamDestroy(s->side);
+    if (s->comm) cudaStreamDestroy(s->comm);
+    if (s->ev_h0) cudaEventDestroy(s->ev_h0);
+    if (s->ev_h1) cudaEventDestroy(s->ev_h1);
     if (s->ev_fork) cudaEventDestroy(s->ev_fork);
     if (s->ev_join) cudaEventDestroy(s->ev_join);
     if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);

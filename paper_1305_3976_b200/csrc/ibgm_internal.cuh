@@ -122,6 +122,12 @@ struct Ctx {
     // it has been done, so X, Uprev, Xh, F and G already belong to the next step
     cudaStream_t side;
     cudaEvent_t ev_fork, ev_join;
+    // z-slabs: the u^{n+1} halos the next step's S1 needs are exchanged on `comm` as soon as
+    // the last Douglas sweep has formed u^{n+1}, concurrently with the psi passes
+    // (ev_h0 fork, ev_h1 join); u_halo_ready: the current u's halo planes are valid
+    cudaStream_t comm;
+    cudaEvent_t ev_h0, ev_h1;
+    bool u_halo_ready;
     bool ib_ahead;
     int lookahead;                    // 1 (default) enables the overlap
     // CUDA graphs of one regular step, per pointer parity (u <-> st, N <-> G swaps) and
@@ -170,6 +176,7 @@ struct Group {
     void* comm;                       // ncclComm_t
     void* comm_side;                  // a second communicator (ncclCommSplit) for the IB
                                       // look-ahead's all-reduce on the side stream
+    void* comm_halo;                  // a third one for the early u halos on the comm stream
     // the viscous cut-axis system's S^{-1} is diagonal to rounding (every off-diagonal
     // entry below 1e-18 of the diagonal): y_t = w0 r_t, so each part needs only its
     // neighbour parts' scalars -- a nearest-neighbour exchange instead of the line masters
@@ -198,7 +205,7 @@ cudaError_t slab_interp_part(Ctx* top, Ctx* s, double* Upart, int* list, int* co
 cudaError_t slab_sum_slots(Ctx* top, const double* part, int P, double* out);
 cudaError_t slab_evolve(Ctx* top, const double* U, int first);   // also keeps X^n, U^{n-1} in Xold, Uold
 cudaError_t slab_spread_part(Ctx* top, Ctx* s, int* list, int* count);
-int group_halo(Group* G, int nf, const HaloSpec* spec, cudaStream_t st);
+int group_halo(Group* G, int nf, const HaloSpec* spec, cudaStream_t st, void* comm = nullptr);
 int group_up(Group* G, int ns, cudaStream_t st);          // scalars to the line masters
 int group_dn(Group* G, int ncomp, cudaStream_t st);       // y and corrections back
 int group_edge(Group* G, int ncomp, cudaStream_t st);     // neighbour parts' scalars (visc_local)

@@ -931,8 +931,9 @@ __global__ void k_halo_copy(const HaloPtrs H, long long PL)
 // Halo exchange of the listed fields.  dir_up: plane nz-1 of slab s
 // -> plane -1 of slab s+1; dir_down: plane 0 of slab s -> plane nz of slab s-1 (periodic).
 // Returns 0, a cudaError_t (as int, transport EMULATE) or an ncclResult_t (NCCL).
-int group_halo(Group* G, int nf, const HaloSpec* spec, cudaStream_t st)
+int group_halo(Group* G, int nf, const HaloSpec* spec, cudaStream_t st, void* comm)
 {
+    if (!comm) comm = G->comm;
     const int P = G->P;
     if (G->transport == IB_TRANSPORT_EMULATE) {
         // the same sends and receives as the NCCL branch below, one launch for all of them
@@ -966,12 +967,12 @@ int group_halo(Group* G, int nf, const HaloSpec* spec, cudaStream_t st)
     for (int f = 0; f < nf; ++f) {
         double* fld = spec[f].field(a);
         if (spec[f].up) {
-            NCK(g_nccl.Send(fld + (nz - 1) * PL, (size_t)PL, kNcclDouble, up, G->comm, st));
-            NCK(g_nccl.Recv(fld - PL, (size_t)PL, kNcclDouble, dn, G->comm, st));
+            NCK(g_nccl.Send(fld + (nz - 1) * PL, (size_t)PL, kNcclDouble, up, comm, st));
+            NCK(g_nccl.Recv(fld - PL, (size_t)PL, kNcclDouble, dn, comm, st));
         }
         if (spec[f].down) {
-            NCK(g_nccl.Send(fld, (size_t)PL, kNcclDouble, dn, G->comm, st));
-            NCK(g_nccl.Recv(fld + nz * PL, (size_t)PL, kNcclDouble, up, G->comm, st));
+            NCK(g_nccl.Send(fld, (size_t)PL, kNcclDouble, dn, comm, st));
+            NCK(g_nccl.Recv(fld + nz * PL, (size_t)PL, kNcclDouble, up, comm, st));
         }
     }
     NCK(g_nccl.GroupEnd());

@@ -265,3 +265,34 @@ def test_divn_handoff_forced_on_a_small_grid():
     r = subprocess.run([sys.executable, "-c", _DIVN_CASE.format(root=root)], capture_output=True, text=True,
                        env=dict(os.environ, IBGM_DIVN="1"), timeout=900)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("cfg,over,P", [(3, dict(n=32, nodes=2000), 4), (0, {}, 2)])
+def test_slab_set_fields_after_steps(cfg, over, P):
+    """On z-slabs the u halos for the next step's S1 are exchanged during the previous
+    step's psi passes (replayed graphs rely on them); ib_set_fields must make the next
+    step exchange them again.  step 5, set_fields(new u, p), step 5 vs the oracle."""
+    from paper_1305_3976_b200 import inputs
+    pr = inputs.config(cfg, **over)
+    o = _oracle_for(pr)
+    g = _gpu(pr, P)
+    o.step(5)
+    g.step(5)
+    rng = np.random.default_rng(12)
+    shp = (pr.n,) * pr.dim
+    u2 = [0.05 * rng.standard_normal(shp) for _ in range(pr.dim)]
+    p2 = 0.1 * rng.standard_normal(shp)
+    if pr.dim == 3:
+        o.set_fields(*u2, p=p2)
+        g.set_fields(*u2, p=p2)
+    else:
+        o.set_fields(u2[0], u2[1], None, p2)
+        g.set_fields(u2[0], u2[1], None, p2)
+    o.step(5)
+    g.step(5)
+    fo, fg = o.fields(), g.fields()
+    for c in range(pr.dim):
+        assert _rel(fg["u"][c], fo["u"][c]) <= 1e-9, c
+    assert _rel(fg["p"], fo["p"]) <= 1e-9
+    assert _rel(fg["X"], fo["X"]) <= 1e-9
+    g.close()
