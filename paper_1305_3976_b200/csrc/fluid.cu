@@ -755,11 +755,18 @@ struct LinePass {
     }
 };
 
-// (not needed when the pass applies the line's S^{-1} in banded or circulant form)
+// doubles of shared memory the staged S^{-1} takes: none when the pass applies the
+// line's S^{-1} in banded or circulant form (the freed space admits more blocks per SM)
+template <int MODES>
+__host__ __device__ __forceinline__ int sinv_slots(const LineCoef& C)
+{
+    return (((MODES & kSchurBand) && C.band >= 0) || ((MODES & kSchurCirc) && C.circ)) ? 0 : C.P * C.P;
+}
+
 template <int MODES>
 __device__ __forceinline__ void load_sinvT(double* sinvT, const SchurInv* SI, const LineCoef& C)
 {
-    if (((MODES & kSchurBand) && C.band >= 0) || ((MODES & kSchurCirc) && C.circ)) return;
+    if (sinv_slots<MODES>(C) == 0) return;
     const int P = C.P;
     for (int e = threadIdx.x; e < P * P; e += blockDim.x) sinvT[e] = SI->sinvT[e];
 }
@@ -774,7 +781,7 @@ __global__ void __launch_bounds__(256, MINB) k_lines(const LineCoef C, const Sch
     const int P = C.P;
     const int TP = tile_pitch(P, L);
     double* sinvT = smem;
-    double* tile = smem + P * P;
+    double* tile = smem + sinv_slots<schur_modes(KIND)>(C);
     double* tile2 = tile + (size_t)NC * R * TP;   // LAST: u^n, PSI_LAST: q (prefetched with the fill)
     load_sinvT<schur_modes(KIND)>(sinvT, SI, C);                     // line factors: not written by the predecessor
     pdl_wait();
@@ -809,7 +816,7 @@ __global__ void __launch_bounds__(32 * WPB, MINB) k_xwarp(const LineCoef C, cons
     constexpr int NT = (KIND == K_PSI_LAST) ? 2 : 1;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double* sinvT = smem;
-    double* tile = smem + P * P + (size_t)w * NT * NC * lpw * TP;
+    double* tile = smem + sinv_slots<schur_modes(KIND)>(C) + (size_t)w * NT * NC * lpw * TP;
     double* tile2 = tile + (size_t)NC * lpw * TP;
     load_sinvT<schur_modes(KIND)>(sinvT, SI, C);
     __syncthreads();
@@ -842,7 +849,7 @@ __global__ void __launch_bounds__(512) k_strided(const LineCoef C, const SchurIn
     extern __shared__ double smem[];
     const int P = C.P;
     double* sinvT = smem;
-    double* xl = sinvT + P * P;          // [P][RI] last interior value f*_{s,m}
+    double* xl = sinvT + sinv_slots<schur_modes(KIND)>(C);   // [P][RI] last interior value f*_{s,m}
     double* rr = xl + P * RI;            // [P][RI] reduced right-hand side r_s
     double* yb = rr + P * RI;            // [P][RI] y_s
     double* ds = yb + P * RI;            // [P][RI] line sums of d (mean correction)
@@ -1087,7 +1094,8 @@ static cudaError_t go_lines(Ctx* s, int sys, const LArgs& a, int ncomp_grid)
                                       : std::max(8, std::min(32, (L > 16 || wide ? 512 : 256) / s->P));
             if (s->n % RI == 0 && s->P * RI <= 512) {
                 auto kern = k_strided<L, KIND, DIM, AX>;
-                const size_t sm = ((size_t)s->P * s->P + 5 * (size_t)s->P * RI) * sizeof(double);
+                const size_t sm = ((size_t)sinv_slots<schur_modes(KIND)>(s->hcoef[sys]) + 5 * (size_t)s->P * RI) *
+                                  sizeof(double);
                 const int gy = (DIM == 3) ? (int)s->nl : 1;
                 const dim3 grid((unsigned)(s->n / RI), (unsigned)gy, (unsigned)ncomp_grid);
                 kern<<<grid, s->P * RI, sm, s->stream>>>(s->hcoef[sys], s->sinv + sys, (int)s->n, RI, la);
@@ -1108,7 +1116,8 @@ static cudaError_t go_lines(Ctx* s, int sys, const LArgs& a, int ncomp_grid)
             const int lpw = 32 / s->P;
             const int TP = tile_pitch(s->P, L);
             const int NT = (KIND == K_PSI_LAST) ? 2 : 1;
-            const size_t sm = ((size_t)s->P * s->P + (size_t)WPB * NT * NC * lpw * TP) * sizeof(double);
+            const size_t sm = ((size_t)sinv_slots<schur_modes(KIND)>(s->hcoef[sys]) + (size_t)WPB * NT * NC * lpw * TP) *
+                              sizeof(double);
             static unsigned long long attr_mask = 0;
             const cudaError_t ae = smem_attr_once(attr_mask, kern, (int)smem_limit());
             if (ae != cudaSuccess) return ae;
@@ -1148,6 +1157,10 @@ static cudaError_t go_lines_k(Ctx* s, int sys, const LArgs& la, int ncomp_grid, 
         }
         if (rk > 0 && lines_smem(s->P, L, tiles_of(KIND, NC), rk) <= 200 * 1024) R = rk;
     }
+    // (the tiled passes keep the S^{-1} space in their allocation even when they do not
+    //  stage it: trimmed, the divergence pass at config 4 runs 4 blocks per SM instead of 3
+    //  and measured 723 -> 824 us; the strided and warp-owned passes gain from the trim:
+    //  y sweep 416 -> 397 us, psi_x 341 -> 334 us)
     const size_t sm = lines_smem(s->P, L, tiles_of(KIND, NC), R);
     static unsigned long long attr_mask = 0;   // per instantiation, per device
     {
