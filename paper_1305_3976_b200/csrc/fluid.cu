@@ -864,7 +864,38 @@ __global__ void __launch_bounds__(512) k_strided(const LineCoef C, const SchurIn
     const unsigned q0 = base + S * (unsigned)(s * L);
     double x[L];
     double un[L];
-    if (KIND == K_DIVPSI) {
+    if (KIND == K_DIVPSI && A.divn) {
+        // D.u^{n+1} at the part's cells with D.u^n from S1: u_AX^{n+1}(I + e_AX) of one cell
+        // is u_AX^{n+1}(I) of the next; every load of the part before the first p store
+        const unsigned stp[3] = {1u, N, N * N};
+        double pq[L];
+        double zc = ldg(pick3<const double*>(A.unew[0], A.unew[1], A.unew[2], AX) + q0);
+#pragma unroll
+        for (int j = 0; j < L; ++j) {
+            const unsigned q = q0 + S * (unsigned)j;
+            int ijk[3];
+            ijk[0] = i;
+            if (AX == 1) { ijk[1] = s * L + j; ijk[2] = 0; } else { ijk[1] = (int)blockIdx.y; ijk[2] = s * L + j; }
+            double dn = 0.0;
+#pragma unroll
+            for (int c = 0; c < DIM; ++c) {
+                const unsigned qp = (ijk[c] == n - 1) ? q - (N - 1) * stp[c] : q + stp[c];
+                const double* unw = pick3<const double*>(A.unew[0], A.unew[1], A.unew[2], c);
+                const double up = ldg(unw + qp);
+                if (c == AX) {
+                    dn += up - zc;
+                    zc = up;
+                } else {
+                    dn += up - ldg(unw + q);
+                }
+            }
+            dn *= A.invh;
+            x[j] = A.neg_rho_dt * dn;
+            pq[j] = A.p[q] - A.chimu_half * (dn + ldg(A.divn + q));
+        }
+#pragma unroll
+        for (int j = 0; j < L; ++j) A.p[q0 + S * (unsigned)j] = pq[j];
+    } else if (KIND == K_DIVPSI) {
         // D.u^{n+1} and D.u^n at the part's cells; Step 3e RHS and the
         // explicit part of Step 3f
         const unsigned stp[3] = {1u, N, N * N};
@@ -1033,6 +1064,20 @@ static bool strided_enabled()
     return v == 1;
 }
 
+// the first psi pass strided when S1 supplies D.u^n: with five u^{n+1} loads per cell
+// (u_z reused along the part) and every load of the part issued before the p stores, the
+// register-resident layout beats the tile (config 4: 731 -> 658 us, 3.996 -> 3.927
+// ms/step).  A/B switch: IBGM_DIV_STRIDED=0 (tiled, contiguous-chunk fill).
+static bool div_strided_enabled()
+{
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("IBGM_DIV_STRIDED");
+        v = (e && atoi(e) == 0) ? 0 : 1;
+    }
+    return v == 1;
+}
+
 static int pick_r(const Ctx* s, int L, int nc, int64_t rows, int64_t other, int per_sm = 0)
 {
     static int forced = -1, mb_env = -1;
@@ -1074,10 +1119,11 @@ static cudaError_t go_lines(Ctx* s, int sys, const LArgs& a, int ncomp_grid)
         }
         la.s1flat = fl;
     }
-    // (the divergence pass stays tiled: strided it measured 35.3 -> 41.4 us at config 3,
-    //  995 -> 1335 us at config 4 -- twelve gathers per cell, all before the solve)
-    if constexpr (AX != 0 && L <= 32 && (KIND == K_MID || KIND == K_LAST)) {
-        if (strided_enabled()) {
+    // (the divergence pass gathering u^n stays tiled: strided it measured 35.3 -> 41.4 us
+    //  at config 3, 995 -> 1335 us at config 4 -- twelve gathers per cell before the solve;
+    //  with D.u^n from S1 it runs strided, see div_strided_enabled)
+    if constexpr (AX != 0 && L <= 32 && (KIND == K_MID || KIND == K_LAST || KIND == K_DIVPSI)) {
+        if (strided_enabled() && (KIND != K_DIVPSI || (la.divn && div_strided_enabled()))) {
             static int ri_env = -1;
             if (ri_env < 0) {
                 const char* e = getenv("IBGM_RI");
@@ -1089,7 +1135,7 @@ static cudaError_t go_lines(Ctx* s, int sys, const LArgs& a, int ncomp_grid)
             // round 2, banded S^{-1} (no staged S^{-1} left in shared memory): the z sweep
             // at P = 32 takes 512 threads, RI 16 (config 4: 750 -> 686 us; y passes 424 ->
             // 431, psi_y 232 -> 243 at RI 16, so they keep RI 8)
-            const bool wide = (KIND == K_LAST && AX == 2 && s->P >= 32);
+            const bool wide = ((KIND == K_LAST || KIND == K_DIVPSI) && AX == 2 && s->P >= 32);
             const int RI = ri_env > 0 ? ri_env
                                       : std::max(8, std::min(32, (L > 16 || wide ? 512 : 256) / s->P));
             if (s->n % RI == 0 && s->P * RI <= 512) {
