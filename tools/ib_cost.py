@@ -2,7 +2,7 @@ import os, sys, json
 sys.path.insert(0, '/root/repo')
 import torch
 from paper_1305_3976_b200 import ibgm, inputs
-for cfg in (4, 3):
+for cfg in [int(a) for a in sys.argv[1:]] or (4, 3):
     for ib in (True, False):
         pr = inputs.config(cfg)
         if not ib:
