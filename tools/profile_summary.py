@@ -67,6 +67,9 @@ with open(os.path.join(out_dir, f"{tag}_launches.txt"), "w") as f:
     for ph, (c, t, nm) in sorted(agg.items(), key=lambda x: -x[1][1]):
         f.write(f"{ph:16s} {c:6d} {t / 1e3:10.1f} {t / c / 1e3:8.2f} {t / tot:7.3f}  {nm}\n")
 
+if rep == "-":          # launch list only (no --set full capture this time)
+    print(open(os.path.join(out_dir, f"{tag}_launches.txt")).read())
+    sys.exit(0)
 M = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
      "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
      "l1tex__throughput.avg.pct_of_peak_sustained_elapsed", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
