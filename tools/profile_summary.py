@@ -15,7 +15,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 tag, lcsv, rep, cfg = sys.argv[1], sys.argv[2], sys.argv[3], sys.argv[4]
-out_dir = os.path.join(ROOT, "profiles")
+out_dir = os.environ.get("PROFILE_OUT") or os.path.join(ROOT, "profiles")
 os.makedirs(out_dir, exist_ok=True)
 
 # phase of a launch: kernel template kind + grid
@@ -47,7 +47,7 @@ def phase_of(name, grid):
             return "psi_x_p"
     return name
 
-rows = [r for r in csv.reader(open(lcsv)) if len(r) > 5]
+rows = [r for r in csv.reader(open(lcsv)) if len(r) > 5] if lcsv != "-" else [["Metric Name"]]
 hdr = rows[0]
 ix = {h: i for i, h in enumerate(hdr)}
 agg = collections.OrderedDict()
@@ -61,7 +61,7 @@ for r in rows[1:]:
     a[0] += 1
     a[1] += v
 tot = sum(v[1] for v in agg.values())
-with open(os.path.join(out_dir, f"{tag}_launches.txt"), "w") as f:
+with open(os.devnull, "w") if lcsv == "-" else open(os.path.join(out_dir, f"{tag}_launches.txt"), "w") as f:
     f.write(f"# ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised): {lcsv}\n")
     f.write("# phase  launches  total_us  avg_us  share_of_all_launches  kernel\n")
     for ph, (c, t, nm) in sorted(agg.items(), key=lambda x: -x[1][1]):
@@ -100,5 +100,4 @@ with open(os.path.join(out_dir, f"{tag}_ncu_full.txt"), "w") as f:
         f.write(f"{ph:16s} | {us:7.1f} | {rd:8.1f} | {wr:8.1f} | {g(M[3]):5.1f} | {g(M[4]):5.1f} | {g(M[5]):5.1f} | "
                 f"{g(M[6]):5.1f} | {g(M[7]):5.1f} | {g(M[8]):4.0f} | {grid}  {nm}\n")
 json.dump(traffic, open(os.path.join(out_dir, f"traffic_cfg{cfg}.json"), "w"), indent=1)
-print(open(os.path.join(out_dir, f"{tag}_launches.txt")).read())
 print(open(os.path.join(out_dir, f"{tag}_ncu_full.txt")).read())
