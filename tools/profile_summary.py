@@ -14,38 +14,12 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 tag, lcsv, rep, cfg = sys.argv[1], sys.argv[2], sys.argv[3], sys.argv[4]
 out_dir = os.environ.get("PROFILE_OUT") or os.path.join(ROOT, "profiles")
 os.makedirs(out_dir, exist_ok=True)
 
-# phase of a launch: kernel template kind + grid
-def phase_of(name, grid):
-    if name.startswith("k_interp"):
-        return "interp_evolve"
-    if name.startswith("k_force"):
-        return "force"
-    if name.startswith("k_spread") or name.startswith("k_brick"):
-        return "spread"
-    if name.startswith("k_xwarp"):
-        # k_xwarp<L, KIND, DIM, NC, WPB, MINB>: x-line passes
-        args = [a.strip() for a in name[name.index("<") + 1:name.index(">")].split(",")]
-        return "s1_rhs_xsweep" if int(args[1]) == 0 else "psi_x_p"
-    if name.startswith("k_lines") or name.startswith("k_strided"):
-        # k_lines<L, KIND, DIM, AX, ...>, k_strided<L, KIND, DIM, AX>
-        args = [a.strip() for a in name[name.index("<") + 1:name.index(">")].split(",")]
-        kind, ax = int(args[1]), int(args[3])
-        if kind == 0:
-            return "s1_rhs_xsweep"
-        if kind == 1:
-            z = grid.split(",")[-1].strip(" )") if grid else "1"
-            return "sweep_y" if z != "1" else "psi_y"
-        if kind == 2:
-            return "sweep_z" if ax == 2 else "sweep_y"
-        if kind == 3:
-            return "div_psi_first"
-        if kind == 4:
-            return "psi_x_p"
-    return name
+from kernel_phase import phase_of  # noqa: E402
 
 rows = [r for r in csv.reader(open(lcsv)) if len(r) > 5] if lcsv != "-" else [["Metric Name"]]
 hdr = rows[0]
