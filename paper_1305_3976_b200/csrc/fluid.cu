@@ -455,6 +455,7 @@ struct LArgs {
     int nl;                 // local planes of the last axis (N, or the slab depth)
     int wrap;               // 1: the last axis is periodic here; 0: z-slab with halo planes
     int s1flat;             // S1 fill flattened over the tile's cells when n >= threads
+    int mfwarp;             // k_strided: mean-correction line sums by warp partials (IBGM_MFWARP=0: off)
 };
 
 // Visit every (line l, position m) of a tile with coalesced global offsets: consecutive
@@ -840,8 +841,15 @@ __global__ void __launch_bounds__(32 * WPB, MINB) k_xwarp(const LineCoef C, cons
 // arithmetic of ws_solve with shared memory in place of the lane shuffles, and no
 // staged tile.
 // -------------------------------------------------------------------------------
+// minimum blocks of 512 threads per SM (register cap 64 / 40) for the passes whose parts
+// fit; 0 leaves the choice to ptxas (the divergence pass and long parts take up to 128)
+__host__ __device__ constexpr int strided_minb(int l, int kind)
+{
+    return (kind == K_MID && l <= 8) ? 3 : (((kind == K_MID && l <= 16) || (kind == K_LAST && l <= 12)) ? 2 : 0);
+}
+
 template <int L, int KIND, int DIM, int AX>
-__global__ void __launch_bounds__(512) k_strided(const LineCoef C, const SchurInv* __restrict__ SI, int n, int RI,
+__global__ void __launch_bounds__(512, strided_minb(L, KIND)) k_strided(const LineCoef C, const SchurInv* __restrict__ SI, int n, int RI,
                                                  LArgs A)
 {
     static_assert(AX != 0, "x lines use the tiled pass");
@@ -850,10 +858,12 @@ __global__ void __launch_bounds__(512) k_strided(const LineCoef C, const SchurIn
     const int P = C.P;
     double* sinvT = smem;
     double* xl = sinvT + sinv_slots<schur_modes(KIND)>(C);   // [P][RI] last interior value f*_{s,m}
-    double* rr = xl + P * RI;            // [P][RI] reduced right-hand side r_s
-    double* yb = rr + P * RI;            // [P][RI] y_s
+    double* yb = xl + P * RI;            // [P][RI] y_s
     double* ds = yb + P * RI;            // [P][RI] line sums of d (mean correction)
     double* xs = ds + P * RI;            // [P][RI] line sums of x
+    double* rr = xs + P * RI;            // [P][RI] reduced right-hand side r_s, every four parts
+                                         // shifted by 8 doubles (rr_at; P RI + 2 P doubles)
+    auto rr_at = [RI](int q, int l) { return q * RI + l + ((q >> 2) << 3); };
     load_sinvT<schur_modes(KIND)>(sinvT, SI, C);
     const int il = threadIdx.x % RI, s = threadIdx.x / RI;
     const int i = blockIdx.x * RI + il;
@@ -943,34 +953,71 @@ __global__ void __launch_bounds__(512) k_strided(const LineCoef C, const SchurIn
     for (int j = M - 1; j >= 1; --j) x[j] -= C.cp[j - 1] * x[j + 1];
     const int sp = (s == 0) ? P - 1 : s - 1, sn = (s == P - 1) ? 0 : s + 1;
     xl[s * RI + il] = x[M];
-    if (mf) ds[s * RI + il] = dsum;
+    // line sums for the mean correction: a warp holds 32 / RI consecutive parts of its RI
+    // lines (lane = (s mod 32/RI) RI + il), so it sums them by shuffles and stores one
+    // partial per (warp, line); each thread then adds P RI / 32 partials instead of P
+    // (psi_y at config 4: 64 -> 16 shared loads per thread; IBGM_MFWARP=0 for A/B)
+    const bool wsum = mf && A.mfwarp && RI <= 32 && (32 % RI) == 0 && ((P * RI) & 31) == 0;
+    const int wq = threadIdx.x >> 5, nwq = (P * RI) >> 5;
+    const bool wlead = (threadIdx.x & 31) < RI;
+    if (wsum) {
+        for (int off = RI; off < 32; off <<= 1) dsum += __shfl_xor_sync(0xffffffffu, dsum, off);
+        if (wlead) ds[wq * RI + il] = dsum;
+    } else if (mf) {
+        ds[s * RI + il] = dsum;
+    }
     __syncthreads();
-    rr[s * RI + il] = x[0] - c * xl[sp * RI + il] - b * x[1];
+    rr[rr_at(s, il)] = x[0] - c * xl[sp * RI + il] - b * x[1];
     __syncthreads();
     double ys = 0.0;
     constexpr int MODES = schur_modes(KIND);
-    if ((MODES & kSchurBand) && C.band >= 0) {
-        // banded circulant S^{-1} (LineCoef::band)
-        ys = C.w[kMaxBand] * rr[s * RI + il];
+    if ((MODES & kSchurCirc) && C.circ && P == kMaxSeg && A.mfwarp >= 2) {
+        // dense circulant S^{-1} at P = 32, register-tiled: the first P/4 RI threads form
+        // four consecutive outputs each from 35 loads of r (y_{s0+j} = sum_d wf[d] r_{s0+j+d},
+        // d ascending as below: the same sums), instead of 32 loads per output in every thread
+        if ((int)threadIdx.x < (kMaxSeg / 4) * RI) {
+            const int s0 = 4 * s;                     // this thread's (il, s) as output group s
+            double y0 = 0.0, y1 = 0.0, y2 = 0.0, y3 = 0.0;
 #pragma unroll
-        for (int d = 1; d <= kMaxBand; ++d) {
-            if (d > C.band) break;
-            const int qp = (s + d >= P) ? s + d - P : s + d, qm = (s - d < 0) ? s - d + P : s - d;
-            ys = fma(C.w[kMaxBand + d], rr[qp * RI + il], ys);
-            ys = fma(C.w[kMaxBand - d], rr[qm * RI + il], ys);
+            for (int k = 0; k < kMaxSeg + 3; ++k) {
+                const int q = (s0 + k >= kMaxSeg) ? s0 + k - kMaxSeg : s0 + k;
+                const double r = rr[rr_at(q, il)];
+                if (k < kMaxSeg) y0 = fma(C.wf[k], r, y0);
+                if (k >= 1 && k - 1 < kMaxSeg) y1 = fma(C.wf[k >= 1 ? k - 1 : 0], r, y1);
+                if (k >= 2 && k - 2 < kMaxSeg) y2 = fma(C.wf[k >= 2 ? k - 2 : 0], r, y2);
+                if (k >= 3) y3 = fma(C.wf[k >= 3 ? k - 3 : 0], r, y3);
+            }
+            yb[(s0 + 0) * RI + il] = y0;
+            yb[(s0 + 1) * RI + il] = y1;
+            yb[(s0 + 2) * RI + il] = y2;
+            yb[(s0 + 3) * RI + il] = y3;
         }
-    } else if ((MODES & kSchurCirc) && C.circ) {
-#pragma unroll
-        for (int d = 0; d < kMaxSeg; ++d) {
-            if (d >= P) break;
-            const int q = (s + d >= P) ? s + d - P : s + d;
-            ys = fma(C.wf[d], rr[q * RI + il], ys);
-        }
+        __syncthreads();
+        ys = yb[s * RI + il];
     } else {
-        for (int q = 0; q < P; ++q) ys = fma(sinvT[q * P + s], rr[q * RI + il], ys);
+        if ((MODES & kSchurBand) && C.band >= 0) {
+            // banded circulant S^{-1} (LineCoef::band)
+            ys = C.w[kMaxBand] * rr[rr_at(s, il)];
+#pragma unroll
+            for (int d = 1; d <= kMaxBand; ++d) {
+                if (d > C.band) break;
+                const int qp = (s + d >= P) ? s + d - P : s + d, qm = (s - d < 0) ? s - d + P : s - d;
+                ys = fma(C.w[kMaxBand + d], rr[rr_at(qp, il)], ys);
+                ys = fma(C.w[kMaxBand - d], rr[rr_at(qm, il)], ys);
+            }
+        } else if ((MODES & kSchurCirc) && C.circ) {
+#pragma unroll
+            for (int d = 0; d < kMaxSeg; ++d) {
+                if (d >= P) break;
+                const int q = (s + d >= P) ? s + d - P : s + d;
+                ys = fma(C.wf[d], rr[rr_at(q, il)], ys);
+            }
+        } else {
+            for (int q = 0; q < P; ++q) ys = fma(sinvT[q * P + s], rr[rr_at(q, il)], ys);
+        }
+        yb[s * RI + il] = ys;
+        __syncthreads();
     }
-    yb[s * RI + il] = ys;
-    __syncthreads();
     const double ys1 = yb[sn * RI + il];
     x[0] = ys;
     const double cy = c * ys, by = b * ys1;
@@ -980,10 +1027,16 @@ __global__ void __launch_bounds__(512) k_strided(const LineCoef C, const SchurIn
         double t = 0.0;
 #pragma unroll
         for (int j = 0; j < L; ++j) t += x[j];
-        xs[s * RI + il] = t;
+        if (wsum) {
+            for (int off = RI; off < 32; off <<= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+            if (wlead) xs[wq * RI + il] = t;
+        } else {
+            xs[s * RI + il] = t;
+        }
         __syncthreads();
         double D = 0.0, X = 0.0;
-        for (int q = 0; q < P; ++q) {
+        const int nq = wsum ? nwq : P;
+        for (int q = 0; q < nq; ++q) {
             D += ds[q * RI + il];
             X += xs[q * RI + il];
         }
@@ -1112,6 +1165,14 @@ static cudaError_t go_lines(Ctx* s, int sys, const LArgs& a, int ncomp_grid)
     la.nl = (int)s->nl;
     la.wrap = s->wrap;
     {
+        static int mw = -1;
+        if (mw < 0) {
+            const char* e = getenv("IBGM_MFWARP");
+            mw = e ? atoi(e) : 2;   // 1: warp partial sums only, 2: + tiled dense circulant S^{-1}
+        }
+        la.mfwarp = mw;
+    }
+    {
         static int fl = -1;
         if (fl < 0) {
             const char* e = getenv("IBGM_S1FLAT");
@@ -1140,7 +1201,7 @@ static cudaError_t go_lines(Ctx* s, int sys, const LArgs& a, int ncomp_grid)
                                       : std::max(8, std::min(32, (L > 16 || wide ? 512 : 256) / s->P));
             if (s->n % RI == 0 && s->P * RI <= 512) {
                 auto kern = k_strided<L, KIND, DIM, AX>;
-                const size_t sm = ((size_t)sinv_slots<schur_modes(KIND)>(s->hcoef[sys]) + 5 * (size_t)s->P * RI) *
+                const size_t sm = ((size_t)sinv_slots<schur_modes(KIND)>(s->hcoef[sys]) + 5 * (size_t)s->P * RI + 2 * (size_t)s->P) *
                                   sizeof(double);
                 const int gy = (DIM == 3) ? (int)s->nl : 1;
                 const dim3 grid((unsigned)(s->n / RI), (unsigned)gy, (unsigned)ncomp_grid);
