@@ -1197,8 +1197,18 @@ static cudaError_t go_lines(Ctx* s, int sys, const LArgs& a, int ncomp_grid)
             // at P = 32 takes 512 threads, RI 16 (config 4: 750 -> 686 us; y passes 424 ->
             // 431, psi_y 232 -> 243 at RI 16, so they keep RI 8)
             const bool wide = ((KIND == K_LAST || KIND == K_DIVPSI) && AX == 2 && s->P >= 32);
-            const int RI = ri_env > 0 ? ri_env
-                                      : std::max(8, std::min(32, (L > 16 || wide ? 512 : 256) / s->P));
+            int RI = ri_env > 0 ? ri_env : std::max(8, std::min(32, (L > 16 || wide ? 512 : 256) / s->P));
+            {
+                // per-kind A/B override: IBGM_RI_K1 (y passes), IBGM_RI_K2 (last sweep), IBGM_RI_K3 (first psi pass)
+                static int rk = -1;
+                if (rk < 0) {
+                    char nm[32];
+                    snprintf(nm, sizeof(nm), "IBGM_RI_K%d", KIND);
+                    const char* e = getenv(nm);
+                    rk = e ? atoi(e) : 0;
+                }
+                if (rk > 0) RI = rk;
+            }
             if (s->n % RI == 0 && s->P * RI <= 512) {
                 auto kern = k_strided<L, KIND, DIM, AX>;
                 const size_t sm = ((size_t)sinv_slots<schur_modes(KIND)>(s->hcoef[sys]) + 5 * (size_t)s->P * RI + 2 * (size_t)s->P) *
