@@ -845,7 +845,9 @@ __global__ void __launch_bounds__(32 * WPB, MINB) k_xwarp(const LineCoef C, cons
 // fit; 0 leaves the choice to ptxas (the divergence pass and long parts take up to 128)
 __host__ __device__ constexpr int strided_minb(int l, int kind)
 {
-    return (kind == K_MID && l <= 8) ? 3 : (((kind == K_MID && l <= 16) || (kind == K_LAST && l <= 12)) ? 2 : 0);
+    return (kind == K_DIVPSI && l <= 16)
+               ? 1   // (all 128 registers: ptxas otherwise stops at 106 and sinks five of the fill's loads below the first store)
+               : ((kind == K_MID && l <= 8) ? 3 : (((kind == K_MID && l <= 16) || (kind == K_LAST && l <= 12)) ? 2 : 0));
 }
 
 template <int L, int KIND, int DIM, int AX>
@@ -863,7 +865,10 @@ __global__ void __launch_bounds__(512, strided_minb(L, KIND)) k_strided(const Li
     double* xs = ds + P * RI;            // [P][RI] line sums of x
     double* rr = xs + P * RI;            // [P][RI] reduced right-hand side r_s, every four parts
                                          // shifted by 8 doubles (rr_at; P RI + 2 P doubles)
-    auto rr_at = [RI](int q, int l) { return q * RI + l + ((q >> 2) << 3); };
+    // (only the kinds that can take the tiled dense circulant form shift r; the last
+    //  viscous sweep keeps the plain [P][RI] indexing and none of the warp-sum code)
+    constexpr bool kTile = (schur_modes(KIND) & kSchurCirc) != 0;
+    auto rr_at = [RI](int q, int l) { return kTile ? q * RI + l + ((q >> 2) << 3) : q * RI + l; };
     load_sinvT<schur_modes(KIND)>(sinvT, SI, C);
     const int il = threadIdx.x % RI, s = threadIdx.x / RI;
     const int i = blockIdx.x * RI + il;
@@ -957,7 +962,7 @@ __global__ void __launch_bounds__(512, strided_minb(L, KIND)) k_strided(const Li
     // lines (lane = (s mod 32/RI) RI + il), so it sums them by shuffles and stores one
     // partial per (warp, line); each thread then adds P RI / 32 partials instead of P
     // (psi_y at config 4: 64 -> 16 shared loads per thread; IBGM_MFWARP=0 for A/B)
-    const bool wsum = mf && A.mfwarp && RI <= 32 && (32 % RI) == 0 && ((P * RI) & 31) == 0;
+    const bool wsum = kTile && mf && A.mfwarp && RI <= 32 && (32 % RI) == 0 && ((P * RI) & 31) == 0;
     const int wq = threadIdx.x >> 5, nwq = (P * RI) >> 5;
     const bool wlead = (threadIdx.x & 31) < RI;
     if (wsum) {
@@ -971,7 +976,8 @@ __global__ void __launch_bounds__(512, strided_minb(L, KIND)) k_strided(const Li
     __syncthreads();
     double ys = 0.0;
     constexpr int MODES = schur_modes(KIND);
-    if ((MODES & kSchurCirc) && C.circ && P == kMaxSeg && A.mfwarp >= 2) {
+    const bool banded = (MODES & kSchurBand) && C.band >= 0;   // (takes precedence: 2 band + 1 taps)
+    if (!banded && (MODES & kSchurCirc) && C.circ && P == kMaxSeg && A.mfwarp >= 2) {
         // dense circulant S^{-1} at P = 32, register-tiled: the first P/4 RI threads form
         // four consecutive outputs each from 35 loads of r (y_{s0+j} = sum_d wf[d] r_{s0+j+d},
         // d ascending as below: the same sums), instead of 32 loads per output in every thread
@@ -995,7 +1001,7 @@ __global__ void __launch_bounds__(512, strided_minb(L, KIND)) k_strided(const Li
         __syncthreads();
         ys = yb[s * RI + il];
     } else {
-        if ((MODES & kSchurBand) && C.band >= 0) {
+        if (banded) {
             // banded circulant S^{-1} (LineCoef::band)
             ys = C.w[kMaxBand] * rr[rr_at(s, il)];
 #pragma unroll
